@@ -35,6 +35,12 @@ extern "C" {
 
 #define CCDK_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define CCDK_API __attribute__((visibility("default")))
+#else
+#define CCDK_API
+#endif
+
 typedef enum {
     CCDK_OK = 0,
     CCDK_INVALID_INPUT = 1, /* ccdkit::InvalidInput (core.hpp:47-53) */
@@ -128,53 +134,53 @@ typedef struct {
 typedef struct ccdk_ctx ccdk_ctx;
 
 /* ---- context ------------------------------------------------------------ */
-int ccdk_abi_version(void);
-const char* ccdk_last_error(void);
-int ccdk_ctx_create(int device, ccdk_ctx** out);
-int ccdk_ctx_destroy(ccdk_ctx* ctx);
+CCDK_API int ccdk_abi_version(void);
+CCDK_API const char* ccdk_last_error(void);
+CCDK_API int ccdk_ctx_create(int device, ccdk_ctx** out);
+CCDK_API int ccdk_ctx_destroy(ccdk_ctx* ctx);
 /* Run all work of this context on `stream` (a cudaStream_t); NULL = own stream. */
-int ccdk_ctx_set_stream(ccdk_ctx* ctx, void* stream);
-int ccdk_ctx_synchronize(ccdk_ctx* ctx);
+CCDK_API int ccdk_ctx_set_stream(ccdk_ctx* ctx, void* stream);
+CCDK_API int ccdk_ctx_synchronize(ccdk_ctx* ctx);
 /* Narrow-phase interval buffer capacity (intervals per generation buffer).
  * 0 = size from free device memory. Exceeding it returns CCDK_CAPACITY. */
-int ccdk_ctx_set_interval_capacity(ccdk_ctx* ctx, uint64_t intervals);
+CCDK_API int ccdk_ctx_set_interval_capacity(ccdk_ctx* ctx, uint64_t intervals);
 
 /* ---- geometry: aabb.hpp ------------------------------------------------- */
 /* round_down_reduced / round_up_reduced (aabb.hpp:10-14, aabb.cpp:10-28),
  * batched; non-finite input -> CCDK_INVALID_INPUT. */
-int ccdk_round_reduced(ccdk_ctx* ctx, const double* x, uint64_t n, float* down, float* up);
+CCDK_API int ccdk_round_reduced(ccdk_ctx* ctx, const double* x, uint64_t n, float* down, float* up);
 
 /* build_boxes (aabb.hpp:49-50, aabb.cpp:71-112).  Scene layout: vertices as
  * nv*3 doubles per snapshot, edges ne*2 u32, faces nf*3 u32.  Outputs k =
  * nv+ne+nf boxes: min/max k*3 floats, owner kind (u8) and index (u32). */
-int ccdk_build_boxes(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+CCDK_API int ccdk_build_boxes(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
                      const uint32_t* edges, uint64_t ne, const uint32_t* faces,
                      uint64_t nf, double inflation, float* min_corner,
                      float* max_corner, uint8_t* owner_kind, uint32_t* owner_index);
 
 /* ---- broad phase: broadphase.hpp ---------------------------------------- */
 /* choose_axis (broadphase.hpp:51, broadphase.cpp:45-67). */
-int ccdk_choose_axis(ccdk_ctx* ctx, const float* min_corner, const float* max_corner,
+CCDK_API int ccdk_choose_axis(ccdk_ctx* ctx, const float* min_corner, const float* max_corner,
                      uint64_t k, int* axis);
 
 /* stq / bf / sap (broadphase.hpp:57-68) over arbitrary boxes.  Result pairs
  * stay on the device in ctx; *n_pairs receives the count, fetch them with
  * ccdk_fetch_pairs.  range_end = UINT64_MAX means unrestricted. */
-int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner,
+CCDK_API int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner,
                      const float* max_corner, const uint8_t* owner_kind,
                      const uint32_t* owner_index, uint64_t k, uint64_t nv,
                      const uint32_t* edges, uint64_t ne, const uint32_t* faces,
                      uint64_t nf, uint64_t range_begin, uint64_t range_end,
                      uint64_t* n_pairs, ccdk_stq_stats* stats);
 /* Copy the last pair list: out holds 2*n_pairs u64 (left id, right id). */
-int ccdk_fetch_pairs(ccdk_ctx* ctx, uint64_t* out);
+CCDK_API int ccdk_fetch_pairs(ccdk_ctx* ctx, uint64_t* out);
 /* Copy StqStats::round_sizes of the last broad phase (n_rounds entries). */
-int ccdk_fetch_round_sizes(ccdk_ctx* ctx, uint64_t* out);
+CCDK_API int ccdk_fetch_round_sizes(ccdk_ctx* ctx, uint64_t* out);
 
 /* classify (broadphase.hpp:78-79, broadphase.cpp:194-239): pairs (2*n u64)
  * -> VF queries then EE queries (pipeline.cpp:162-165 order).  Output
  * arrays must hold n entries; *n_vf and *n_ee receive the counts. */
-int ccdk_classify(ccdk_ctx* ctx, const uint64_t* pairs, uint64_t n_pairs,
+CCDK_API int ccdk_classify(ccdk_ctx* ctx, const uint64_t* pairs, uint64_t n_pairs,
                   const double* v0, const double* v1, uint64_t nv,
                   const uint32_t* edges, uint64_t ne, const uint32_t* faces,
                   uint64_t nf, uint8_t* kind_out, double* points_out,
@@ -183,13 +189,13 @@ int ccdk_classify(ccdk_ctx* ctx, const uint64_t* pairs, uint64_t n_pairs,
 /* ---- narrow phase: narrowphase.hpp ------------------------------------- */
 /* inclusion_box (narrowphase.hpp:59) batched: box = (tlo,thi,ulo,uhi,vlo,vhi)
  * per entry; out = 6 doubles (x.lo,x.hi,y.lo,y.hi,z.lo,z.hi). */
-int ccdk_inclusion_boxes(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+CCDK_API int ccdk_inclusion_boxes(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
                          const double* boxes, uint64_t n, double* out);
 
 /* process_interval (narrowphase.hpp:77-79) batched.  depth = 3 u16 per box;
  * sep < 0 means cfg.min_separation.  action[i] in CCDK_ACTION_*; for Split,
  * children = 12 doubles (left box, right box) and child_depth = 6 u16. */
-int ccdk_process_intervals(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+CCDK_API int ccdk_process_intervals(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
                            const double* boxes, const uint16_t* depth,
                            const double* t_star, const double* sep, uint64_t n,
                            const ccdk_narrow_cfg* cfg, uint8_t* action,
@@ -201,7 +207,7 @@ int ccdk_process_intervals(ccdk_ctx* ctx, const uint8_t* kind, const double* poi
  * tolerance_hit, bit1 = zero_toi_diagnostic).  queue_capacity = UINT64_MAX
  * for unbounded.  On semantic overflow stats->overflow = 1 and per-query
  * results are the defaults, as in the reference. */
-int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+CCDK_API int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
                       const double* per_query_sep, uint64_t n,
                       const ccdk_narrow_cfg* cfg, uint64_t queue_capacity,
                       double* toi, uint8_t* flags, ccdk_narrow_stats* stats);
@@ -211,26 +217,26 @@ int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
  * buffers (H2D copy, box build, broad phase, classify, narrow phase, global
  * min, D2H of the report).  Candidates stay on the device: fetch with
  * ccdk_fetch_pairs (report->candidate_count pairs, canonical order). */
-int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+CCDK_API int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
              const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
              const ccdk_pipeline_cfg* cfg, ccdk_report* report);
 
 /* Device-resident variant: upload a scene once, then run steps on it. */
-int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+CCDK_API int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
                       const uint32_t* edges, uint64_t ne, const uint32_t* faces,
                       uint64_t nf);
 /* Full step on the uploaded scene.  shard_count > 1 restricts the sweep to
  * this shard's slice of sorted left positions (equal pair-test work per
  * shard, SweepRange semantics of broadphase.hpp:37-43); the caller combines
  * shards with an allreduce(min) of report->toi. */
-int ccdk_ccd_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shard_rank,
+CCDK_API int ccdk_ccd_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shard_rank,
                       uint32_t shard_count, ccdk_report* report);
 /* Device pointer (double) holding the last step's global ToI, for a
  * device-side allreduce(min) by the multi-GPU host layer. */
-int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr);
+CCDK_API int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr);
 
 /* Per-query results of the last ccd step (query_count entries). */
-int ccdk_fetch_query_results(ccdk_ctx* ctx, double* toi, uint8_t* flags);
+CCDK_API int ccdk_fetch_query_results(ccdk_ctx* ctx, double* toi, uint8_t* flags);
 
 #ifdef __cplusplus
 }

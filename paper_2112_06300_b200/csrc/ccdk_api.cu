@@ -1,0 +1,999 @@
+// The C ABI (include/ccdk.h): context, validation, the reference-facing entry
+// points and the device-resident full CCD step (pipeline.cpp:179-232).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "ccdk_internal.cuh"
+
+namespace ccdk {
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(ccdk_ctx* ctx, F&& f)
+{
+    try {
+        f();
+        return CCDK_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = e.what();
+        return CCDK_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return CCDK_CUDA;
+    }
+    (void)ctx;
+}
+
+template <typename T>
+T* grow(DevBuf& b, uint64_t n)
+{
+    return static_cast<T*>(b.ensure(n * sizeof(T)));
+}
+
+void h2d(Ctx& c, void* dst, const void* src, size_t bytes)
+{
+    if (bytes)
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.stream));
+}
+
+void d2h(Ctx& c, void* dst, const void* src, size_t bytes)
+{
+    if (bytes)
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+}
+
+void sync(Ctx& c) { CCDK_CUDA_CHECK(cudaStreamSynchronize(c.stream)); }
+
+// ---- SceneStep::validate (scene.cpp:13-34) on the device.  Codes follow the
+// reference's check order so the first failing check is reported.
+enum : unsigned long long {
+    kErrNone = ~0ull,
+    kErrNonFinite = 1,
+    kErrEdgeRange = 2,
+    kErrEdgeSame = 3,
+    kErrFaceRange = 4,
+    kErrFaceSame = 5,
+};
+
+const char* scene_error_text(unsigned long long code)
+{
+    switch (code) {
+    case kErrNonFinite:
+        return "non-finite vertex coordinate";
+    case kErrEdgeRange:
+        return "edge index out of range";
+    case kErrEdgeSame:
+        return "edge endpoints must be distinct";
+    case kErrFaceRange:
+        return "face index out of range";
+    case kErrFaceSame:
+        return "face vertices must be distinct";
+    }
+    return "invalid scene";
+}
+
+__global__ void k_validate_scene(const double* v0, const double* v1, unsigned long long nv,
+                                 const uint32_t* e, unsigned long long ne, const uint32_t* f,
+                                 unsigned long long nf, unsigned long long* err)
+{
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < 3 * nv + ne + nf; i += stride) {
+        unsigned long long code = kErrNone;
+        if (i < 3 * nv) {
+            if (!isfinite(v0[i]) || !isfinite(v1[i]))
+                code = kErrNonFinite;
+        } else if (i < 3 * nv + ne) {
+            const unsigned long long j = i - 3 * nv;
+            const uint32_t a = e[2 * j], b = e[2 * j + 1];
+            if (a >= nv || b >= nv)
+                code = kErrEdgeRange;
+            else if (a == b)
+                code = kErrEdgeSame;
+        } else {
+            const unsigned long long j = i - 3 * nv - ne;
+            const uint32_t a = f[3 * j], b = f[3 * j + 1], d = f[3 * j + 2];
+            if (a >= nv || b >= nv || d >= nv)
+                code = kErrFaceRange;
+            else if (a == b || b == d || a == d)
+                code = kErrFaceSame;
+        }
+        if (code != kErrNone)
+            atomicMin(err, code);
+    }
+}
+
+// ---- general-box broad phase helpers (arbitrary owners)
+
+__global__ void k_owner_keys(const uint8_t* kind, const uint32_t* index, unsigned long long k,
+                             unsigned long long* keys, uint32_t* pos)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= k)
+        return;
+    keys[i] = (static_cast<unsigned long long>(kind[i]) << 32) | index[i];
+    pos[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_rank_flags(const unsigned long long* skeys, unsigned long long k, uint32_t* flag)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= k)
+        return;
+    flag[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1u : 0u;
+}
+
+// Gather boxes into owner order: SoA corners, vertex triple + dense rank, raw
+// position; owner tables by rank.  Owner indices are range-checked (the
+// reference's share_vertex would index out of bounds).
+__global__ void k_gather_general(const float* mn, const float* mx, const uint8_t* kind,
+                                 const uint32_t* index, const uint32_t* order,
+                                 const uint32_t* rank_incl, unsigned long long k,
+                                 unsigned long long nv, const uint32_t* e, unsigned long long ne,
+                                 const uint32_t* f, unsigned long long nf, float* bmin,
+                                 float* bmax, uint4* vids, uint32_t* raw, uint8_t* own_kind,
+                                 uint32_t* own_index, unsigned long long* err)
+{
+    const unsigned long long s = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (s >= k)
+        return;
+    const unsigned long long r = order[s];
+    for (int c = 0; c < 3; ++c) {
+        bmin[c * k + s] = mn[3 * r + c];
+        bmax[c * k + s] = mx[3 * r + c];
+    }
+    const uint8_t kd = kind[r];
+    const uint32_t ix = index[r];
+    const uint32_t rank = rank_incl[s] - 1;
+    uint4 w = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, rank);
+    bool bad = false;
+    if (kd == CCDK_KIND_VERTEX) {
+        w.x = ix; // share_vertex compares the index itself (scene.cpp:58-60)
+    } else if (kd == CCDK_KIND_EDGE) {
+        if (ix < ne) {
+            w.x = e[2ull * ix];
+            w.y = e[2ull * ix + 1];
+        } else {
+            bad = true;
+        }
+    } else if (kd == CCDK_KIND_FACE) {
+        if (ix < nf) {
+            w.x = f[3ull * ix];
+            w.y = f[3ull * ix + 1];
+            w.z = f[3ull * ix + 2];
+        } else {
+            bad = true;
+        }
+    } else {
+        bad = true;
+    }
+    if (bad)
+        atomicMin(err, s);
+    vids[s] = w;
+    raw[s] = static_cast<uint32_t>(r);
+    own_kind[rank] = kd;
+    own_index[rank] = ix;
+}
+
+__global__ void k_aos_to_soa(const float* mn, const float* mx, unsigned long long k, float* bmin,
+                             float* bmax)
+{
+    const unsigned long long s = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (s >= k)
+        return;
+    for (int c = 0; c < 3; ++c) {
+        bmin[c * k + s] = mn[3 * s + c];
+        bmax[c * k + s] = mx[3 * s + c];
+    }
+}
+
+// ---- classify over arbitrary pair lists (broadphase.cpp:194-239)
+__global__ void k_classify_flags(const unsigned long long* pairs, unsigned long long n,
+                                 unsigned long long nv, const uint32_t* e, unsigned long long ne,
+                                 const uint32_t* f, unsigned long long nf, uint32_t* fvf,
+                                 uint32_t* fee, unsigned long long* err)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= n)
+        return;
+    const unsigned long long a = pairs[2 * i], b = pairs[2 * i + 1];
+    const unsigned ka = static_cast<unsigned>(a >> 32), kb = static_cast<unsigned>(b >> 32);
+    const uint32_t ia = static_cast<uint32_t>(a), ib = static_cast<uint32_t>(b);
+    const auto limit = [&](unsigned kd) { return kd == 0 ? nv : kd == 1 ? ne : nf; };
+    uint32_t vf = 0, ee = 0;
+    if (ka > 2 || kb > 2 || ia >= limit(ka) || ib >= limit(kb)) {
+        atomicMin(err, i);
+    } else if (ka == CCDK_KIND_VERTEX && kb == CCDK_KIND_FACE) {
+        vf = (ia != f[3ull * ib] && ia != f[3ull * ib + 1] && ia != f[3ull * ib + 2]) ? 1u : 0u;
+    } else if (ka == CCDK_KIND_EDGE && kb == CCDK_KIND_EDGE) {
+        const uint32_t a0 = e[2ull * ia], a1 = e[2ull * ia + 1], b0 = e[2ull * ib], b1 = e[2ull * ib + 1];
+        ee = (a0 != b0 && a0 != b1 && a1 != b0 && a1 != b1) ? 1u : 0u;
+    }
+    fvf[i] = vf;
+    fee[i] = ee;
+}
+
+__global__ void k_classify_write(const unsigned long long* pairs, unsigned long long n,
+                                 const uint32_t* fvf, const uint32_t* fee, const uint32_t* ovf,
+                                 const uint32_t* oee, const unsigned long long* n_vf_ptr,
+                                 const double* v0, const double* v1, const uint32_t* e,
+                                 const uint32_t* f, uint8_t* kind, double* pts,
+                                 unsigned long long* src)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= n || !(fvf[i] | fee[i]))
+        return;
+    const unsigned long long a = pairs[2 * i], b = pairs[2 * i + 1];
+    const uint32_t ia = static_cast<uint32_t>(a), ib = static_cast<uint32_t>(b);
+    uint32_t pv[4];
+    unsigned long long q;
+    if (fvf[i]) {
+        q = ovf[i];
+        pv[0] = ia;
+        pv[1] = f[3ull * ib];
+        pv[2] = f[3ull * ib + 1];
+        pv[3] = f[3ull * ib + 2];
+        kind[q] = CCDK_QUERY_VF;
+    } else {
+        q = *n_vf_ptr + oee[i];
+        pv[0] = e[2ull * ia];
+        pv[1] = e[2ull * ia + 1];
+        pv[2] = e[2ull * ib];
+        pv[3] = e[2ull * ib + 1];
+        kind[q] = CCDK_QUERY_EE;
+    }
+    for (int p = 0; p < 4; ++p)
+        for (int c = 0; c < 3; ++c) {
+            pts[24 * q + 3 * p + c] = v0[3ull * pv[p] + c];
+            pts[24 * q + 12 + 3 * p + c] = v1[3ull * pv[p] + c];
+        }
+    src[2 * q] = a;
+    src[2 * q + 1] = b;
+}
+
+__global__ void k_count_total(const uint32_t* flags, const uint32_t* offs, unsigned long long n,
+                              unsigned long long* out)
+{
+    *out = n ? static_cast<unsigned long long>(offs[n - 1]) + flags[n - 1] : 0;
+}
+
+__global__ void k_count_vf(const unsigned long long* keys, unsigned long long n, int nb,
+                           unsigned long long nv, unsigned long long* out)
+{
+    // keys are sorted: VF keys (lo rank < nv) form a prefix
+    unsigned long long a = 0, b = n;
+    while (a < b) {
+        const unsigned long long m = (a + b) >> 1;
+        if ((keys[m] >> nb) < nv)
+            a = m + 1;
+        else
+            b = m;
+    }
+    *out = a;
+}
+
+__global__ void k_store_toi(const NarrowScalars* sc, int have_queries, double* out)
+{
+    *out = have_queries ? __longlong_as_double(static_cast<long long>(sc->global_toi_bits))
+                        : CUDART_INF;
+}
+
+template <typename F>
+void cub_call(Ctx& c, F&& f)
+{
+    size_t bytes = 0;
+    CCDK_CUDA_CHECK(f(nullptr, bytes));
+    void* tmp = c.cub_tmp.ensure(bytes);
+    CCDK_CUDA_CHECK(f(tmp, bytes));
+}
+
+void validate_narrow_cfg(const ccdk_narrow_cfg& c)
+{
+    // NarrowConfig::validate, narrowphase.cpp:10-20
+    if (!(c.delta > 0.0))
+        throw Error(CCDK_CONFIG, "NarrowConfig: delta must be > 0");
+    if (c.max_splits < 1)
+        throw Error(CCDK_CONFIG, "NarrowConfig: max_splits must be >= 1");
+    if (c.min_separation < 0.0)
+        throw Error(CCDK_CONFIG, "NarrowConfig: min_separation must be >= 0");
+    if (!(c.t_max > 0.0) || c.t_max > 1.0)
+        throw Error(CCDK_CONFIG, "NarrowConfig: t_max must be in (0, 1]");
+}
+
+void validate_pipeline_cfg(const ccdk_pipeline_cfg& p)
+{
+    // PipelineConfig::validate, pipeline.cpp:23-37
+    validate_narrow_cfg(p.narrow);
+    if (p.rs_params == 0 || p.rs_query == 0 || p.rs_interval == 0 || p.rs_pair_ints == 0)
+        throw Error(CCDK_CONFIG, "PipelineConfig: record sizes must be positive");
+    if (p.memory_budget <= p.rs_params)
+        throw Error(CCDK_CONFIG, "PipelineConfig: memory budget must exceed the parameter size");
+    if (p.min_sep_fraction < 0.0)
+        throw Error(CCDK_CONFIG, "PipelineConfig: min_sep_fraction must be >= 0");
+    if (p.threads < 1)
+        throw Error(CCDK_CONFIG, "PipelineConfig: threads must be >= 1");
+    if (p.inflation < 0.0)
+        throw Error(CCDK_CONFIG, "PipelineConfig: inflation must be >= 0");
+}
+
+void validate_scene_dev(Ctx& c)
+{
+    DevScene& s = c.scene;
+    auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
+    CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->misc[3], 0xff, 8, c.stream));
+    const uint64_t n = 3 * s.nv + s.ne + s.nf;
+    if (n) {
+        k_validate_scene<<<std::min<unsigned>(grid_for(n, 256).x, 8u * c.num_sms), 256, 0, c.stream>>>(
+            s.v0.as<double>(), s.v1.as<double>(), s.nv, s.edges.as<uint32_t>(), s.ne,
+            s.faces.as<uint32_t>(), s.nf, &ctr->misc[3]);
+        CCDK_LAUNCH_CHECK();
+    }
+}
+
+void check_scene_error(Ctx& c)
+{
+    auto* ctr = c.counters.as<DevCounters>();
+    unsigned long long code = 0;
+    d2h(c, &code, &ctr->misc[3], 8);
+    sync(c);
+    if (code != kErrNone)
+        throw Error(CCDK_INVALID_INPUT, scene_error_text(code));
+}
+
+// Upload a scene into ctx.scene and validate it on the device
+// (SceneStep::validate, scene.cpp:13-34) before any kernel indexes it.
+void upload_scene(Ctx& c, const double* v0, const double* v1, uint64_t nv, const uint32_t* e,
+                  uint64_t ne, const uint32_t* f, uint64_t nf)
+{
+    DevScene& s = c.scene;
+    s.valid = false;
+    s.nv = nv;
+    s.ne = ne;
+    s.nf = nf;
+    h2d(c, s.v0.ensure(nv * 24), v0, nv * 24);
+    h2d(c, s.v1.ensure(nv * 24), v1, nv * 24);
+    h2d(c, s.edges.ensure(ne * 8), e, ne * 8);
+    h2d(c, s.faces.ensure(nf * 12), f, nf * 12);
+    validate_scene_dev(c);
+    check_scene_error(c);
+    s.valid = true;
+}
+
+// The full CCD step on ctx.scene (pipeline.cpp:218-232 via run_batched at the
+// default budget): build -> STQ -> classify -> narrow -> global min.
+void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_t shard_count,
+              ccdk_report& rep, cudaEvent_t start_event)
+{
+    validate_pipeline_cfg(cfg);
+    if (cfg.min_sep_mode == CCDK_MINSEP_RELATIVE)
+        throw Error(CCDK_CONFIG, "ccdk_ccd: Relative min-separation is not implemented on the device path yet");
+    DevScene& s = c.scene;
+    std::memset(&rep, 0, sizeof rep);
+    rep.toi = INFINITY;
+    rep.batch_count = 1;
+    const uint64_t k = s.nv + s.ne + s.nf;
+    cudaStream_t st = c.stream;
+    cudaEvent_t ev[6];
+    for (auto& e : ev)
+        CCDK_CUDA_CHECK(cudaEventCreate(&e));
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[0], st));
+
+    // K1 (the scene was validated when it was uploaded)
+    float* bmin = grow<float>(c.bmin, 3 * std::max<uint64_t>(k, 1));
+    float* bmax = grow<float>(c.bmax, 3 * std::max<uint64_t>(k, 1));
+    uint4* vids = grow<uint4>(c.vids, std::max<uint64_t>(k, 1));
+    launch_build_boxes(c, s.v0.as<double>(), s.v1.as<double>(), s.nv, s.edges.as<uint32_t>(), s.ne,
+                       s.faces.as<uint32_t>(), s.nf, cfg.inflation, bmin, bmax, vids);
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[1], st));
+    // K2-K6
+    BroadIn bi;
+    bi.bmin = bmin;
+    bi.bmax = bmax;
+    bi.vids = vids;
+    bi.k = k;
+    bi.method = CCDK_BROAD_STQ; // stq/sap/bf give the identical set on a full range
+    bi.shard_rank = shard_rank;
+    bi.shard_count = shard_count;
+    BroadOut bo;
+    broad_phase(c, bi, bo);
+    {
+        auto* ctr = c.counters.as<DevCounters>();
+        unsigned long long err = 0;
+        d2h(c, &err, &ctr->error, 8);
+        sync(c);
+        if (k && err != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
+    }
+    c.last_pairs_general = false;
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[2], st));
+    // K7
+    const uint64_t n = bo.n_pairs;
+    uint8_t* qk = grow<uint8_t>(c.q_kind, std::max<uint64_t>(n, 1));
+    double* qp = grow<double>(c.q_points, 24 * std::max<uint64_t>(n, 1));
+    const uint64_t* keys = c.pair_keys_sorted.as<uint64_t>();
+    launch_classify_keys(c, keys, n, c.last_nb, s.v0.as<double>(), s.v1.as<double>(), s.nv,
+                         s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp);
+    auto* ctr = c.counters.as<DevCounters>();
+    if (n)
+        k_count_vf<<<1, 1, 0, st>>>(reinterpret_cast<const unsigned long long*>(keys), n,
+                                    c.last_nb, s.nv, &ctr->misc[2]);
+    CCDK_LAUNCH_CHECK();
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[3], st));
+    // K8 + K9
+    NarrowIn ni;
+    ni.kind = qk;
+    ni.points = qp;
+    ni.n = n;
+    ni.cfg = cfg.narrow;
+    NarrowOut no;
+    narrow_phase(c, ni, no);
+    c.last_query_count = n;
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[4], st));
+    double* dtoi = grow<double>(c.last_toi, 1);
+    k_store_toi<<<1, 1, 0, st>>>(static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars))),
+                                 n ? 1 : 0, dtoi);
+    CCDK_LAUNCH_CHECK();
+    unsigned long long any_flags = 0, vf_count = 0;
+    if (n) {
+        auto* sc = c.nscal.as<NarrowScalars>();
+        d2h(c, &any_flags, &sc->any_flags, 8);
+        d2h(c, &vf_count, &ctr->misc[2], 8);
+    }
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[5], st));
+    CCDK_CUDA_CHECK(cudaEventSynchronize(ev[5]));
+
+    rep.toi = n ? no.stats.global_toi : INFINITY;
+    rep.tolerance_hit = (any_flags & CCDK_FLAG_TOLERANCE_HIT) ? 1 : 0;
+    rep.zero_toi_diagnostic = (any_flags & CCDK_FLAG_ZERO_TOI_DIAG) ? 1 : 0;
+    rep.candidate_count = n;
+    rep.query_count = n;
+    rep.vf_count = vf_count;
+    rep.pair_tests = bo.pair_tests;
+    rep.total_splits = no.stats.total_splits;
+    rep.peak_queue = n ? no.stats.peak_queue : 0;
+    rep.evaluations = no.stats.evaluations;
+    rep.split_actions = no.stats.split_actions;
+    rep.generations = no.stats.generations;
+    rep.axis = bo.axis;
+    // tracked_peak_bytes with the reference's accounting (pipeline.cpp:132-136,
+    // 158-159, 228): boxes 32 B, pairs 16 B, queries 216 B, intervals 64+152 B
+    const uint64_t base = k * 32 + n * 16;
+    uint64_t peak = std::max<uint64_t>(k * 32, base);
+    if (n)
+        peak = std::max<uint64_t>(peak, base + n * 216 + rep.peak_queue * (64 + 152));
+    rep.tracked_peak_bytes = peak;
+    float ms[6] = {};
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[0], ev[0], ev[1]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[1], ev[1], ev[2]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[2], ev[2], ev[3]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[3], ev[3], ev[4]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[4], start_event ? start_event : ev[0], ev[5]));
+    rep.ms_build = ms[0];
+    rep.ms_sort = bo.ms_axis_sort;
+    rep.ms_sweep = bo.ms_sweep;
+    rep.ms_pairsort = bo.ms_pairsort;
+    rep.ms_classify = ms[2];
+    rep.ms_narrow = ms[3];
+    rep.ms_total = ms[4];
+    rep.t_cb = ms[0] * 1e-3;
+    rep.t_bp = ms[1] * 1e-3;
+    rep.t_socd = ms[2] * 1e-3;
+    rep.t_np = ms[3] * 1e-3;
+    for (auto& e : ev)
+        cudaEventDestroy(e);
+}
+
+} // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+} // namespace ccdk
+
+using namespace ccdk;
+
+struct ccdk_ctx : Ctx {
+};
+
+extern "C" {
+
+int ccdk_abi_version(void) { return CCDK_ABI_VERSION; }
+
+const char* ccdk_last_error(void) { return g_last_error.c_str(); }
+
+int ccdk_ctx_create(int device, ccdk_ctx** out)
+{
+    return guard(nullptr, [&] {
+        if (!out)
+            throw Error(CCDK_CONFIG, "ccdk_ctx_create: null output");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error(CCDK_CUDA, "no CUDA device available (the ccdk path has no CPU fallback)");
+        if (device < 0 || device >= ndev)
+            throw Error(CCDK_CONFIG, "ccdk_ctx_create: device index out of range");
+        CCDK_CUDA_CHECK(cudaSetDevice(device));
+        std::unique_ptr<ccdk_ctx> c(new ccdk_ctx());
+        c->device = device;
+        CCDK_CUDA_CHECK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        CCDK_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        *out = c.release();
+    });
+}
+
+int ccdk_ctx_destroy(ccdk_ctx* ctx)
+{
+    return guard(ctx, [&] {
+        if (!ctx)
+            return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->own_stream)
+            cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int ccdk_ctx_set_stream(ccdk_ctx* ctx, void* stream)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (ctx->own_stream)
+            CCDK_CUDA_CHECK(cudaStreamDestroy(ctx->stream));
+        if (stream) {
+            ctx->stream = static_cast<cudaStream_t>(stream);
+            ctx->own_stream = false;
+        } else {
+            CCDK_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+    });
+}
+
+int ccdk_ctx_synchronize(ccdk_ctx* ctx)
+{
+    return guard(ctx, [&] { CCDK_CUDA_CHECK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int ccdk_ctx_set_interval_capacity(ccdk_ctx* ctx, uint64_t intervals)
+{
+    return guard(ctx, [&] { ctx->interval_capacity = intervals; });
+}
+
+int ccdk_round_reduced(ccdk_ctx* ctx, const double* x, uint64_t n, float* down, float* up)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        double* dx = grow<double>(c.tmp[0], n);
+        float* dd = grow<float>(c.tmp[1], n);
+        float* du = grow<float>(c.tmp[2], n);
+        h2d(c, dx, x, n * 8);
+        launch_round(c, dx, n, dd, du);
+        d2h(c, down, dd, n * 4);
+        d2h(c, up, du, n * 4);
+        sync(c);
+    });
+}
+
+int ccdk_build_boxes(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+                     const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
+                     double inflation, float* min_corner, float* max_corner, uint8_t* owner_kind,
+                     uint32_t* owner_index)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
+        if (inflation < 0.0)
+            throw Error(CCDK_INVALID_INPUT, "build_boxes: inflation must be >= 0");
+        const uint64_t k = nv + ne + nf;
+        if (!k)
+            return;
+        float* bmin = grow<float>(c.bmin, 3 * k);
+        float* bmax = grow<float>(c.bmax, 3 * k);
+        uint4* vids = grow<uint4>(c.vids, k);
+        launch_build_boxes(c, c.scene.v0.as<double>(), c.scene.v1.as<double>(), nv,
+                           c.scene.edges.as<uint32_t>(), ne, c.scene.faces.as<uint32_t>(), nf,
+                           inflation, bmin, bmax, vids);
+        unsigned long long err = 0;
+        d2h(c, &err, &c.counters.as<DevCounters>()->error, 8);
+        float* mn = grow<float>(c.tmp[0], 3 * k);
+        float* mx = grow<float>(c.tmp[1], 3 * k);
+        uint8_t* kd = grow<uint8_t>(c.tmp[2], k);
+        uint32_t* ix = grow<uint32_t>(c.tmp[3], k);
+        launch_soa_to_aos(c, bmin, bmax, k, mn, mx, kd, ix, nv, ne);
+        d2h(c, min_corner, mn, 12 * k);
+        d2h(c, max_corner, mx, 12 * k);
+        d2h(c, owner_kind, kd, k);
+        d2h(c, owner_index, ix, 4 * k);
+        sync(c);
+        if (err != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
+    });
+}
+
+int ccdk_choose_axis(ccdk_ctx* ctx, const float* min_corner, const float* max_corner, uint64_t k,
+                     int* axis)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (k == 0)
+            throw Error(CCDK_INVALID_INPUT, "choose_axis: empty box list");
+        float* mn = grow<float>(c.tmp[0], 3 * k);
+        float* mx = grow<float>(c.tmp[1], 3 * k);
+        h2d(c, mn, min_corner, 12 * k);
+        h2d(c, mx, max_corner, 12 * k);
+        float* bmin = grow<float>(c.bmin, 3 * k);
+        float* bmax = grow<float>(c.bmax, 3 * k);
+        k_aos_to_soa<<<grid_for(k, 256), 256, 0, c.stream>>>(mn, mx, k, bmin, bmax);
+        CCDK_LAUNCH_CHECK();
+        // reuse the broad phase's K2 by running it on a 1-row range
+        uint4* vids = grow<uint4>(c.vids, k);
+        CCDK_CUDA_CHECK(cudaMemsetAsync(vids, 0xff, k * sizeof(uint4), c.stream));
+        if (k < 2) {
+            *axis = 0; // a single box has zero variance on every axis -> x
+            return;
+        }
+        BroadIn bi;
+        bi.bmin = bmin;
+        bi.bmax = bmax;
+        bi.vids = vids;
+        bi.k = k;
+        bi.range_begin = 0;
+        bi.range_end = 0; // empty sweep: only K2/K3 run
+        BroadOut bo;
+        broad_phase(c, bi, bo);
+        *axis = bo.axis;
+    });
+}
+
+int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner, const float* max_corner,
+                     const uint8_t* owner_kind, const uint32_t* owner_index, uint64_t k,
+                     uint64_t nv, const uint32_t* edges, uint64_t ne, const uint32_t* faces,
+                     uint64_t nf, uint64_t range_begin, uint64_t range_end, uint64_t* n_pairs,
+                     ccdk_stq_stats* stats)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (method < 0 || method > 2)
+            throw Error(CCDK_CONFIG, "broad phase: unknown method");
+        *n_pairs = 0;
+        if (stats)
+            std::memset(stats, 0, sizeof *stats);
+        c.last_n_pairs = 0;
+        c.last_rounds.clear();
+        c.last_pairs_general = true;
+        if (k < 2)
+            return;
+        cudaStream_t s = c.stream;
+        float* mn = grow<float>(c.tmp[0], 3 * k);
+        float* mx = grow<float>(c.tmp[1], 3 * k);
+        uint8_t* kd = grow<uint8_t>(c.tmp[2], k);
+        uint32_t* ix = grow<uint32_t>(c.tmp[3], k);
+        h2d(c, mn, min_corner, 12 * k);
+        h2d(c, mx, max_corner, 12 * k);
+        h2d(c, kd, owner_kind, k);
+        h2d(c, ix, owner_index, 4 * k);
+        uint32_t* e = grow<uint32_t>(c.scene.edges, 2 * std::max<uint64_t>(ne, 1));
+        uint32_t* f = grow<uint32_t>(c.scene.faces, 3 * std::max<uint64_t>(nf, 1));
+        h2d(c, e, edges, 8 * ne);
+        h2d(c, f, faces, 12 * nf);
+        c.scene.valid = false; // only topology was uploaded
+        // owner order + dense ranks
+        unsigned long long* okeys = grow<unsigned long long>(c.tmp[4], 2 * k);
+        uint32_t* pos = grow<uint32_t>(c.tmp[5], 2 * k);
+        k_owner_keys<<<grid_for(k, 256), 256, 0, s>>>(kd, ix, k, okeys, pos);
+        CCDK_LAUNCH_CHECK();
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, okeys, okeys + k, pos, pos + k,
+                                                   static_cast<int64_t>(k), 0, 34, s);
+        });
+        uint32_t* flag = grow<uint32_t>(c.tmp[6], 2 * k);
+        k_rank_flags<<<grid_for(k, 256), 256, 0, s>>>(okeys + k, k, flag);
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceScan::InclusiveSum(t, b, flag, flag + k, static_cast<int64_t>(k), s);
+        });
+        float* bmin = grow<float>(c.bmin, 3 * k);
+        float* bmax = grow<float>(c.bmax, 3 * k);
+        uint4* vids = grow<uint4>(c.vids, k);
+        uint32_t* raw = grow<uint32_t>(c.raw, 2 * k);
+        uint8_t* own_kind = grow<uint8_t>(c.own_kind, k);
+        uint32_t* own_index = grow<uint32_t>(c.own_index, k);
+        auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
+        CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->error, 0xff, 8, s));
+        k_gather_general<<<grid_for(k, 256), 256, 0, s>>>(mn, mx, kd, ix, pos + k, flag + k, k, nv, e,
+                                                          ne, f, nf, bmin, bmax, vids, raw,
+                                                          own_kind, own_index, &ctr->error);
+        CCDK_LAUNCH_CHECK();
+        uint32_t nranks = 0;
+        unsigned long long err = 0;
+        d2h(c, &nranks, flag + 2 * k - 1, 4);
+        d2h(c, &err, &ctr->error, 8);
+        sync(c);
+        if (err != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "broad phase: box owner index out of range");
+        BroadIn bi;
+        bi.bmin = bmin;
+        bi.bmax = bmax;
+        bi.vids = vids;
+        bi.raw = raw;
+        bi.k = k;
+        bi.method = method;
+        bi.range_begin = range_begin;
+        bi.range_end = range_end;
+        bi.want_rounds = stats != nullptr && method == CCDK_BROAD_STQ;
+        bi.unique = nranks < k;
+        BroadOut bo;
+        broad_phase(c, bi, bo);
+        c.last_pairs_general = true;
+        *n_pairs = bo.n_pairs;
+        if (stats) {
+            stats->n_rounds = c.last_rounds.size();
+            stats->max_queue = c.last_rounds.empty() ? 0 : c.last_rounds[0];
+            stats->pair_tests = bo.pair_tests;
+            stats->axis = static_cast<uint64_t>(bo.axis);
+        }
+    });
+}
+
+int ccdk_fetch_pairs(ccdk_ctx* ctx, uint64_t* out)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        const uint64_t n = c.last_n_pairs;
+        if (!n)
+            return;
+        uint64_t* ids = grow<uint64_t>(c.tmp[7], 2 * n);
+        launch_keys_to_ids(c, c.pair_keys_sorted.as<uint64_t>(), n, c.last_nb,
+                           c.last_pairs_general ? c.own_kind.as<uint8_t>() : nullptr,
+                           c.last_pairs_general ? c.own_index.as<uint32_t>() : nullptr,
+                           c.scene.nv, c.scene.ne, ids);
+        d2h(c, out, ids, 16 * n);
+        sync(c);
+    });
+}
+
+int ccdk_fetch_round_sizes(ccdk_ctx* ctx, uint64_t* out)
+{
+    return guard(ctx, [&] {
+        std::copy(ctx->last_rounds.begin(), ctx->last_rounds.end(), out);
+    });
+}
+
+int ccdk_classify(ccdk_ctx* ctx, const uint64_t* pairs, uint64_t n_pairs, const double* v0,
+                  const double* v1, uint64_t nv, const uint32_t* edges, uint64_t ne,
+                  const uint32_t* faces, uint64_t nf, uint8_t* kind_out, double* points_out,
+                  uint64_t* source_out, uint64_t* n_vf, uint64_t* n_ee)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        *n_vf = *n_ee = 0;
+        if (!n_pairs)
+            return;
+        cudaStream_t s = c.stream;
+        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
+        unsigned long long* dp = grow<unsigned long long>(c.tmp[0], 2 * n_pairs);
+        h2d(c, dp, pairs, 16 * n_pairs);
+        uint32_t* fl = grow<uint32_t>(c.tmp[1], 4 * n_pairs);
+        uint32_t *fvf = fl, *fee = fl + n_pairs, *ovf = fl + 2 * n_pairs, *oee = fl + 3 * n_pairs;
+        auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
+        CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->error, 0xff, 8, s));
+        k_classify_flags<<<grid_for(n_pairs, 256), 256, 0, s>>>(dp, n_pairs, nv, c.scene.edges.as<uint32_t>(),
+                                                               ne, c.scene.faces.as<uint32_t>(), nf,
+                                                               fvf, fee, &ctr->error);
+        CCDK_LAUNCH_CHECK();
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, fvf, ovf, static_cast<int64_t>(n_pairs), s);
+        });
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, fee, oee, static_cast<int64_t>(n_pairs), s);
+        });
+        k_count_total<<<1, 1, 0, s>>>(fvf, ovf, n_pairs, &ctr->misc[0]);
+        k_count_total<<<1, 1, 0, s>>>(fee, oee, n_pairs, &ctr->misc[1]);
+        uint8_t* qk = grow<uint8_t>(c.q_kind, n_pairs);
+        double* qp = grow<double>(c.q_points, 24 * n_pairs);
+        unsigned long long* src = grow<unsigned long long>(c.tmp[2], 2 * n_pairs);
+        k_classify_write<<<grid_for(n_pairs, 128), 128, 0, s>>>(
+            dp, n_pairs, fvf, fee, ovf, oee, &ctr->misc[0], c.scene.v0.as<double>(),
+            c.scene.v1.as<double>(), c.scene.edges.as<uint32_t>(), c.scene.faces.as<uint32_t>(), qk,
+            qp, src);
+        CCDK_LAUNCH_CHECK();
+        unsigned long long hc[8];
+        d2h(c, hc, ctr, sizeof hc);
+        sync(c);
+        if (hc[3] != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "classify: primitive index out of range");
+        const uint64_t m = hc[4] + hc[5];
+        *n_vf = hc[4];
+        *n_ee = hc[5];
+        d2h(c, kind_out, qk, m);
+        d2h(c, points_out, qp, 24 * 8 * m);
+        d2h(c, source_out, src, 16 * m);
+        sync(c);
+    });
+}
+
+int ccdk_inclusion_boxes(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+                         const double* boxes, uint64_t n, double* out)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (!n)
+            return;
+        uint8_t* dk = grow<uint8_t>(c.tmp[0], n);
+        double* dp = grow<double>(c.tmp[1], 24 * n);
+        double* db = grow<double>(c.tmp[2], 6 * n);
+        double* dout = grow<double>(c.tmp[3], 6 * n);
+        h2d(c, dk, kind, n);
+        h2d(c, dp, points, 192 * n);
+        h2d(c, db, boxes, 48 * n);
+        launch_inclusion(c, dk, dp, db, n, dout);
+        d2h(c, out, dout, 48 * n);
+        sync(c);
+    });
+}
+
+int ccdk_process_intervals(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+                           const double* boxes, const uint16_t* depth, const double* t_star,
+                           const double* sep, uint64_t n, const ccdk_narrow_cfg* cfg,
+                           uint8_t* action, double* candidate_t, uint8_t* zero_diag,
+                           double* children, uint16_t* child_depth)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (!n)
+            return;
+        uint8_t* dk = grow<uint8_t>(c.tmp[0], n);
+        double* dp = grow<double>(c.tmp[1], 24 * n);
+        double* db = grow<double>(c.tmp[2], 6 * n);
+        uint16_t* dd = grow<uint16_t>(c.tmp[3], 3 * n);
+        double* dts = grow<double>(c.tmp[4], 2 * n);
+        double* dsep = sep ? dts + n : nullptr;
+        uint8_t* dact = grow<uint8_t>(c.tmp[5], 2 * n);
+        double* dct = grow<double>(c.tmp[6], 13 * n);
+        double* dch = dct + n;
+        uint16_t* dcd = grow<uint16_t>(c.tmp[7], 6 * n);
+        h2d(c, dk, kind, n);
+        h2d(c, dp, points, 192 * n);
+        h2d(c, db, boxes, 48 * n);
+        h2d(c, dd, depth, 6 * n);
+        h2d(c, dts, t_star, 8 * n);
+        if (sep)
+            h2d(c, dsep, sep, 8 * n);
+        launch_process(c, dk, dp, db, dd, dts, dsep, n, *cfg, dact, dct, dact + n, dch, dcd);
+        d2h(c, action, dact, n);
+        d2h(c, zero_diag, dact + n, n);
+        d2h(c, candidate_t, dct, 8 * n);
+        d2h(c, children, dch, 96 * n);
+        d2h(c, child_depth, dcd, 12 * n);
+        sync(c);
+    });
+}
+
+int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+                      const double* per_query_sep, uint64_t n, const ccdk_narrow_cfg* cfg,
+                      uint64_t queue_capacity, double* toi, uint8_t* flags,
+                      ccdk_narrow_stats* stats)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        validate_narrow_cfg(*cfg);
+        std::memset(stats, 0, sizeof *stats);
+        stats->global_toi = INFINITY;
+        if (!n)
+            return;
+        uint8_t* dk = grow<uint8_t>(c.q_kind, n);
+        double* dp = grow<double>(c.q_points, 24 * n);
+        double* ds = per_query_sep ? grow<double>(c.q_sep, n) : nullptr;
+        h2d(c, dk, kind, n);
+        h2d(c, dp, points, 192 * n);
+        if (ds)
+            h2d(c, ds, per_query_sep, 8 * n);
+        NarrowIn ni;
+        ni.kind = dk;
+        ni.points = dp;
+        ni.sep = ds;
+        ni.n = n;
+        ni.cfg = *cfg;
+        ni.queue_capacity = queue_capacity;
+        NarrowOut no;
+        narrow_phase(c, ni, no);
+        d2h(c, toi, no.toi, 8 * n);
+        d2h(c, flags, no.flags, n);
+        sync(c);
+        *stats = no.stats;
+    });
+}
+
+int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+                      const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
+        upload_scene(*ctx, v0, v1, nv, edges, ne, faces, nf);
+        sync(*ctx);
+    });
+}
+
+int ccdk_ccd_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shard_rank,
+                      uint32_t shard_count, ccdk_report* report)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (!ctx->scene.valid)
+            throw Error(CCDK_CONFIG, "ccdk_ccd_resident: no scene uploaded");
+        if (shard_count < 1 || shard_rank >= shard_count)
+            throw Error(CCDK_CONFIG, "ccdk_ccd_resident: bad shard");
+        ccd_step(*ctx, *cfg, shard_rank, shard_count, *report, nullptr);
+    });
+}
+
+int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+             const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
+             const ccdk_pipeline_cfg* cfg, ccdk_report* report)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        validate_pipeline_cfg(*cfg);
+        if (!v0 || !v1) {
+            if (nv)
+                throw Error(CCDK_INVALID_INPUT, "vertex snapshots missing");
+        }
+        cudaEvent_t start;
+        CCDK_CUDA_CHECK(cudaEventCreate(&start));
+        CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
+        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
+        ccd_step(c, *cfg, 0, 1, *report, start);
+        cudaEventDestroy(start);
+    });
+}
+
+int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr)
+{
+    return guard(ctx, [&] { *dev_ptr = grow<double>(ctx->last_toi, 1); });
+}
+
+int ccdk_fetch_query_results(ccdk_ctx* ctx, double* toi, uint8_t* flags)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        const uint64_t n = c.last_query_count;
+        d2h(c, toi, c.out_toi.p, 8 * n);
+        d2h(c, flags, c.out_flags.p, n);
+        sync(c);
+    });
+}
+
+} // extern "C"

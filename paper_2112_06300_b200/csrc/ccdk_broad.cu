@@ -1,0 +1,677 @@
+// K2-K6: Sweep-and-Tiniest-Queue broad phase (proj/src/broadphase.cpp:12-192).
+//
+//   K2 choose_axis   deterministic fp64 tree reduction of centre sums and
+//                    squared deviations, strict '>' argmax (broadphase.cpp:45-67)
+//   K3 sort          CUB onesweep radix sort of (orderable min-key, slot):
+//                    stable, -0 == +0, ties by slot = owner order
+//                    (broadphase.cpp:23-35); then a gather into sorted SoA
+//   K4 run ends      U[p] = first q > p with min[q] > max[p] (binary search):
+//                    the STQ queue holds (p, j) in round j-p-1 for exactly the
+//                    j in (p, U[p]), so StqStats follow from run lengths and a
+//                    prefix sum partitions equal pair-test work per shard
+//   K5 sweep         CTA = 128 consecutive left rows; the union of their
+//                    j-windows is staged through shared memory in 256-box
+//                    tiles and read as broadcasts; a warp skips tiles none of
+//                    its rows need; hits (rare) run keep_pair (type + shared
+//                    vertex, broadphase.cpp:12-20) and append u64 pair keys
+//                    with one warp-aggregated atomic per ballot.  Rows whose
+//                    window exceeds CAP spill the remainder as SEG-sized
+//                    segments handled warp-per-segment (load balance for the
+//                    static floor / container walls whose window is ~k).
+//   K6 pair sort     CUB radix sort of (lo_rank << nb | hi_rank) over 2*nb bits
+//                    = canonical CandidatePair order (finalize, 37-41).
+#include <math_constants.h>
+
+#include <cub/cub.cuh>
+
+#include "ccdk_internal.cuh"
+
+namespace ccdk {
+
+namespace {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kTB = 128;        // left rows per sweep CTA
+constexpr int kTile = 256;      // staged boxes per tile
+constexpr uint32_t kCap = 4096; // per-row window handled by the tile kernel
+constexpr uint32_t kSeg = 2048; // heavy-row segment length
+constexpr int kRedBlocks = 256;
+constexpr int kRedThreads = 256;
+
+// ------------------------------------------------------------------- K2
+
+__device__ __forceinline__ double centre(const float* bmin, const float* bmax, unsigned long long k,
+                                         int c, unsigned long long s)
+{
+    return __ddiv_rn(__dadd_rn(static_cast<double>(bmin[c * k + s]),
+                               static_cast<double>(bmax[c * k + s])),
+                     2.0);
+}
+
+// Fixed-shape deterministic block reduction of 3 doubles.
+__device__ void block_sum3(double v[3], double* out)
+{
+    __shared__ double sh[3][kRedThreads];
+    for (int c = 0; c < 3; ++c)
+        sh[c][threadIdx.x] = v[c];
+    __syncthreads();
+    for (int w = kRedThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int c = 0; c < 3; ++c)
+                sh[c][threadIdx.x] = __dadd_rn(sh[c][threadIdx.x], sh[c][threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int c = 0; c < 3; ++c)
+            out[c] = sh[c][0];
+}
+
+__device__ void mean_from_partials(const double* part, unsigned long long k, double mean[3])
+{
+    double v[3] = { 0, 0, 0 };
+    for (int b = threadIdx.x; b < kRedBlocks; b += kRedThreads)
+        for (int c = 0; c < 3; ++c)
+            v[c] = __dadd_rn(v[c], part[3 * b + c]);
+    __shared__ double m[3];
+    block_sum3(v, m);
+    __syncthreads();
+    for (int c = 0; c < 3; ++c)
+        mean[c] = __ddiv_rn(m[c], static_cast<double>(k));
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_axis_sum(const float* bmin, const float* bmax,
+                                                          unsigned long long k, double* part)
+{
+    double v[3] = { 0, 0, 0 };
+    for (unsigned long long s = blockIdx.x * kRedThreads + threadIdx.x; s < k;
+         s += kRedBlocks * kRedThreads)
+        for (int c = 0; c < 3; ++c)
+            v[c] = __dadd_rn(v[c], centre(bmin, bmax, k, c, s));
+    block_sum3(v, part + 3 * blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_axis_var(const float* bmin, const float* bmax,
+                                                          unsigned long long k, const double* part,
+                                                          double* vpart)
+{
+    double mean[3];
+    mean_from_partials(part, k, mean);
+    double v[3] = { 0, 0, 0 };
+    for (unsigned long long s = blockIdx.x * kRedThreads + threadIdx.x; s < k;
+         s += kRedBlocks * kRedThreads)
+        for (int c = 0; c < 3; ++c) {
+            const double d = __dsub_rn(centre(bmin, bmax, k, c, s), mean[c]);
+            v[c] = __dadd_rn(v[c], __dmul_rn(d, d));
+        }
+    __syncthreads();
+    block_sum3(v, vpart + 3 * blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_axis_pick(const double* vpart, int* axis)
+{
+    double v[3] = { 0, 0, 0 };
+    for (int b = threadIdx.x; b < kRedBlocks; b += kRedThreads)
+        for (int c = 0; c < 3; ++c)
+            v[c] = __dadd_rn(v[c], vpart[3 * b + c]);
+    __shared__ double var[3];
+    block_sum3(v, var);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int c = 1; c < 3; ++c)
+            if (var[c] > var[a])
+                a = c;
+        *axis = a;
+    }
+}
+
+// ------------------------------------------------------------------- K3
+
+__device__ __forceinline__ uint32_t orderable(float x)
+{
+    uint32_t u = __float_as_uint(x);
+    if (u == 0x80000000u)
+        u = 0; // -0 == +0 under the reference's float comparator
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void k_sort_keys(const float* bmin, unsigned long long k, const int* axis,
+                            uint32_t* keys, uint32_t* vals)
+{
+    const unsigned long long s = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (s >= k)
+        return;
+    keys[s] = orderable(bmin[static_cast<unsigned long long>(*axis) * k + s]);
+    vals[s] = static_cast<uint32_t>(s);
+}
+
+__global__ void k_permute(const float* bmin, const float* bmax, const uint4* vids,
+                          const uint32_t* raw, unsigned long long k, const int* axis,
+                          const uint32_t* order, float* smin_a, float* smax_a, float4* sbox,
+                          uint4* svid, uint32_t* sraw)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (p >= k)
+        return;
+    const int a = *axis, a1 = (a + 1) % 3, a2 = (a + 2) % 3;
+    const unsigned long long s = order[p];
+    smin_a[p] = bmin[a * k + s];
+    smax_a[p] = bmax[a * k + s];
+    sbox[p] = make_float4(bmin[a1 * k + s], bmax[a1 * k + s], bmin[a2 * k + s], bmax[a2 * k + s]);
+    svid[p] = vids[s];
+    if (sraw)
+        sraw[p] = raw ? raw[s] : static_cast<uint32_t>(s);
+}
+
+// ------------------------------------------------------------------- K4
+
+__global__ void k_run_ends(const float* smin_a, const float* smax_a, unsigned long long k,
+                           unsigned long long lo, unsigned long long hi, uint32_t* run_end,
+                           unsigned long long* run_len, unsigned long long* pair_tests)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    unsigned long long len = 0;
+    if (p < k) {
+        unsigned long long end = p + 1;
+        if (p >= lo && p < hi) {
+            const float reach = smax_a[p];
+            unsigned long long a = p + 1, b = k;
+            while (a < b) { // upper_bound of reach in smin_a[p+1, k)
+                const unsigned long long m = (a + b) >> 1;
+                if (smin_a[m] <= reach)
+                    a = m + 1;
+                else
+                    b = m;
+            }
+            end = a;
+            len = end - p - 1;
+        }
+        run_end[p] = static_cast<uint32_t>(end);
+        if (run_len)
+            run_len[p] = len;
+    }
+    const unsigned long long s = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(len > 0xffffffffull ? 0xffffffffu : len));
+    if ((threadIdx.x & 31) == 0 && s)
+        atomicAdd(pair_tests, s);
+}
+
+// shard boundaries: first p with exclusive prefix >= W*r/S
+__global__ void k_shard_range(const unsigned long long* incl, unsigned long long lo,
+                              unsigned long long hi, uint32_t rank, uint32_t count,
+                              unsigned long long* range)
+{
+    if (threadIdx.x > 1)
+        return;
+    const unsigned long long W = hi > lo ? incl[hi - 1] : 0;
+    const uint32_t r = rank + threadIdx.x;
+    unsigned long long pos;
+    if (r == 0) {
+        pos = lo;
+    } else if (r >= count) {
+        pos = hi;
+    } else {
+        const unsigned long long T = (W / count) * r + ((W % count) * r) / count; // floor(W*r/S)
+        // exclusive prefix E[p] = incl[p] - len(p) = incl[p-1]; find first p in
+        // [lo, hi) with E[p] >= T, i.e. first p with (p == lo ? 0 : incl[p-1]) >= T
+        unsigned long long a = lo, b = hi;
+        while (a < b) {
+            const unsigned long long m = (a + b) >> 1;
+            const unsigned long long e = m == lo ? 0 : incl[m - 1];
+            if (e >= T)
+                b = m;
+            else
+                a = m + 1;
+        }
+        pos = a;
+    }
+    range[threadIdx.x] = pos;
+}
+
+__global__ void k_full_range(unsigned long long lo, unsigned long long hi, unsigned long long* range)
+{
+    range[0] = lo;
+    range[1] = hi;
+}
+
+__global__ void k_heavy_count(const uint32_t* run_end, const unsigned long long* range,
+                              unsigned long long k, uint32_t* nseg)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (p >= k)
+        return;
+    uint32_t n = 0;
+    if (p >= range[0] && p < range[1]) {
+        const unsigned long long start = p + 1 + kCap;
+        const unsigned long long end = run_end[p];
+        if (end > start)
+            n = static_cast<uint32_t>((end - start + kSeg - 1) / kSeg);
+    }
+    nseg[p] = n;
+}
+
+struct Seg {
+    uint32_t p, jb, je, pad;
+};
+
+__global__ void k_heavy_gen(const uint32_t* run_end, const uint32_t* nseg, const uint32_t* off,
+                            unsigned long long k, Seg* segs, unsigned long long* n_heavy)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (p >= k)
+        return;
+    const uint32_t n = nseg[p];
+    if (p == k - 1)
+        *n_heavy = static_cast<unsigned long long>(off[p]) + n;
+    if (!n)
+        return;
+    const uint32_t start = static_cast<uint32_t>(p + 1 + kCap);
+    const uint32_t end = run_end[p];
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t jb = start + i * kSeg;
+        const uint32_t je = min(end, jb + kSeg);
+        segs[off[p] + i] = { static_cast<uint32_t>(p), jb, je, 0 };
+    }
+}
+
+// ------------------------------------------------------------------- K5
+
+struct SweepArgs {
+    const float* smin_a;
+    const float* smax_a;
+    const float4* sbox;
+    const uint4* svid;
+    const uint32_t* sraw;      // bf mode only
+    const uint32_t* run_end;
+    const unsigned long long* range;
+    unsigned long long row0;   // first row covered by the grid
+    unsigned long long k;
+    int nb;
+    int bf;                    // bf: raw-position range filter + full axis test
+    unsigned long long bf_lo, bf_hi;
+    unsigned long long* keys;
+    unsigned long long cap;
+    unsigned long long* n_pairs;
+    const Seg* segs;
+    const unsigned long long* n_heavy;
+};
+
+// keep_pair (broadphase.cpp:12-20) on vertex triples: the count of present
+// vertices is the primitive kind (1 V, 2 E, 3 F).
+__device__ __forceinline__ bool keep_pair(uint4 a, uint4 b)
+{
+    const int na = 1 + (a.y != kNone) + (a.z != kNone);
+    const int nb = 1 + (b.y != kNone) + (b.z != kNone);
+    if (na + nb == 4) {
+        if (na != 2) { // vertex-face
+            const uint32_t v = na == 1 ? a.x : b.x;
+            const uint4 f = na == 1 ? b : a;
+            return v != f.x && v != f.y && v != f.z;
+        }
+        return a.x != b.x && a.x != b.y && a.y != b.x && a.y != b.y; // edge-edge
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool box_hit(float4 m, float4 o)
+{
+    return o.x <= m.y && m.x <= o.y && o.z <= m.w && m.z <= o.w;
+}
+
+__device__ __forceinline__ void emit(const SweepArgs& a, bool keep, uint32_t ra, uint32_t rb)
+{
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (!mask)
+        return;
+    const unsigned lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == static_cast<unsigned>(leader))
+        base = atomicAdd(a.n_pairs, static_cast<unsigned long long>(__popc(mask)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (keep) {
+        const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1));
+        if (slot < a.cap) {
+            const uint32_t lo = min(ra, rb), hi = max(ra, rb);
+            a.keys[slot] = (static_cast<unsigned long long>(lo) << a.nb) | hi;
+        }
+    }
+}
+
+__device__ __forceinline__ bool bf_ok(const SweepArgs& a, unsigned long long p, unsigned long long j)
+{
+    if (!a.bf)
+        return true;
+    const uint32_t r = min(a.sraw[p], a.sraw[j]);
+    return r >= a.bf_lo && r < a.bf_hi && a.smin_a[p] <= a.smax_a[j];
+}
+
+__global__ void __launch_bounds__(kTB) k_sweep_tile(SweepArgs a)
+{
+    __shared__ float4 s_box[kTile];
+    __shared__ uint4 s_vid[kTile];
+    __shared__ unsigned s_span;
+    const unsigned long long B = a.range[0], E = a.range[1];
+    const unsigned long long base = a.row0 + static_cast<unsigned long long>(blockIdx.x) * kTB;
+    if (base >= E || base + kTB <= B)
+        return;
+    const unsigned long long p = base + threadIdx.x;
+    const bool row = p >= B && p < E;
+    float4 mb = make_float4(0, 0, 0, 0);
+    uint4 mv = make_uint4(0, 0, 0, 0);
+    unsigned long long je = p + 1;
+    if (row) {
+        mb = a.sbox[p];
+        mv = a.svid[p];
+        je = min(static_cast<unsigned long long>(a.run_end[p]), p + 1 + kCap);
+    }
+    if (threadIdx.x == 0)
+        s_span = 0;
+    __syncthreads();
+    // window offsets relative to `base` fit in 32 bits (< kTB + kCap + 1)
+    const unsigned jb_off = static_cast<unsigned>(p + 1 - base);
+    const unsigned je_off = static_cast<unsigned>(je - base);
+    if (row && je_off > jb_off)
+        atomicMax(&s_span, je_off);
+    const unsigned w_lo = __reduce_min_sync(0xffffffffu, (row && je_off > jb_off) ? jb_off : 0xffffffffu);
+    const unsigned w_hi = __reduce_max_sync(0xffffffffu, (row && je_off > jb_off) ? je_off : 0u);
+    __syncthreads();
+    const unsigned span = s_span;
+    for (unsigned c0 = 1; c0 < span; c0 += kTile) {
+        const unsigned n = min(static_cast<unsigned>(kTile), span - c0);
+        for (unsigned t = threadIdx.x; t < n; t += kTB) {
+            s_box[t] = a.sbox[base + c0 + t];
+            s_vid[t] = a.svid[base + c0 + t];
+        }
+        __syncthreads();
+        const unsigned j0 = max(c0, w_lo), j1 = min(c0 + n, w_hi);
+        for (unsigned j = j0; j < j1; ++j) {
+            const float4 o = s_box[j - c0];
+            const bool hit = j >= jb_off && j < je_off && box_hit(mb, o);
+            if (__any_sync(0xffffffffu, hit)) {
+                const uint4 ov = s_vid[j - c0];
+                const bool keep = hit && keep_pair(mv, ov) && bf_ok(a, p, base + j);
+                emit(a, keep, mv.w, ov.w);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Heavy rows: one warp per (row, SEG-long window segment), coalesced loads.
+__global__ void __launch_bounds__(256) k_sweep_heavy(SweepArgs a)
+{
+    const unsigned long long nseg = *a.n_heavy;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long warp = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5;
+    const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
+    for (unsigned long long s = warp; s < nseg; s += nwarps) {
+        const Seg g = a.segs[s];
+        const float4 mb = a.sbox[g.p];
+        const uint4 mv = a.svid[g.p];
+        for (uint32_t j0 = g.jb; j0 < g.je; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            bool hit = false;
+            float4 o;
+            if (j < g.je) {
+                o = a.sbox[j];
+                hit = box_hit(mb, o);
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                uint4 ov = make_uint4(0, 0, 0, 0);
+                if (hit)
+                    ov = a.svid[j];
+                const bool keep = hit && keep_pair(mv, ov) && bf_ok(a, g.p, j);
+                emit(a, keep, mv.w, ov.w);
+            }
+        }
+    }
+}
+
+// ---- stats: StqStats::round_sizes[r] = #{i : run_len(i) >= r+1}
+
+__global__ void k_run_hist(const unsigned long long* run_len, unsigned long long k,
+                           unsigned long long* hist, unsigned long long* max_run)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (p >= k)
+        return;
+    const unsigned long long l = run_len[p];
+    if (l) {
+        atomicAdd(&hist[l], 1ull);
+        atomicMax(max_run, l);
+    }
+}
+
+__global__ void k_reverse(const unsigned long long* in, unsigned long long n, unsigned long long off,
+                          unsigned long long* out)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i < n)
+        out[i] = in[off - i];
+}
+
+template <typename T>
+T* grow(DevBuf& b, uint64_t n)
+{
+    return static_cast<T*>(b.ensure(n * sizeof(T)));
+}
+
+template <typename F>
+void cub_call(Ctx& c, F&& f)
+{
+    size_t bytes = 0;
+    CCDK_CUDA_CHECK(f(nullptr, bytes));
+    void* tmp = c.cub_tmp.ensure(bytes);
+    CCDK_CUDA_CHECK(f(tmp, bytes));
+}
+
+} // namespace
+
+void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
+{
+    cudaStream_t s = c.stream;
+    const uint64_t k = in.k;
+    out = BroadOut {};
+    c.last_n_pairs = 0;
+    c.last_rounds.clear();
+    if (k < 2)
+        return; // no pairs (broadphase.cpp:74-76; bf has no j > i either)
+    if (k >= 0xffffffffull)
+        throw Error(CCDK_CONFIG, "broad phase: more than 2^32-2 boxes");
+
+    cudaEvent_t ev[4];
+    for (auto& e : ev)
+        CCDK_CUDA_CHECK(cudaEventCreate(&e));
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[0], s));
+
+    auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
+    // clear the sweep counters; `error` belongs to the box build and is kept
+    CCDK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), s));
+    CCDK_CUDA_CHECK(cudaMemsetAsync(ctr->misc, 0, sizeof ctr->misc, s));
+
+    // K2 choose_axis
+    int* d_axis = static_cast<int*>(c.axis.ensure(64));
+    double* part = grow<double>(c.partials, 6 * kRedBlocks);
+    k_axis_sum<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, part);
+    k_axis_var<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, part, part + 3 * kRedBlocks);
+    k_axis_pick<<<1, kRedThreads, 0, s>>>(part + 3 * kRedBlocks, d_axis);
+    CCDK_LAUNCH_CHECK();
+
+    // K3 sort + permute
+    uint32_t* keys_in = grow<uint32_t>(c.sort_keys_in, k);
+    uint32_t* keys_out = grow<uint32_t>(c.sort_keys_out, k);
+    uint32_t* vals_in = grow<uint32_t>(c.sort_vals_in, k);
+    uint32_t* order = grow<uint32_t>(c.sort_vals_out, k);
+    k_sort_keys<<<grid_for(k, 256), 256, 0, s>>>(in.bmin, k, d_axis, keys_in, vals_in);
+    CCDK_LAUNCH_CHECK();
+    cub_call(c, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, keys_in, keys_out, vals_in, order,
+                                               static_cast<int64_t>(k), 0, 32, s);
+    });
+    float* smin_a = grow<float>(c.smin_a, k);
+    float* smax_a = grow<float>(c.smax_a, k);
+    float4* sbox = grow<float4>(c.sbox, k);
+    uint4* svid = grow<uint4>(c.svid, k);
+    const bool bf = in.method == CCDK_BROAD_BF;
+    uint32_t* sraw = bf ? grow<uint32_t>(c.raw, 2 * k) + k : nullptr;
+    k_permute<<<grid_for(k, 256), 256, 0, s>>>(in.bmin, in.bmax, in.vids, in.raw, k, d_axis, order,
+                                               smin_a, smax_a, sbox, svid, sraw);
+    CCDK_LAUNCH_CHECK();
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[1], s));
+
+    // K4 run ends over the left range (stq/sap: sorted positions; bf: all,
+    // filtered by raw position at emission)
+    uint64_t lo = 0, hi = k - 1;
+    if (!bf) {
+        lo = std::min<uint64_t>(in.range_begin, k - 1);
+        hi = std::min<uint64_t>(in.range_end, k - 1);
+    }
+    uint32_t* run_end = grow<uint32_t>(c.run_end, k);
+    const bool need_len = in.want_rounds || in.shard_count > 1;
+    unsigned long long* run_len = need_len ? grow<unsigned long long>(c.prefix, 2 * k) : nullptr;
+    k_run_ends<<<grid_for(k, 256), 256, 0, s>>>(smin_a, smax_a, k, lo, hi, run_end, run_len,
+                                                 &ctr->pair_tests);
+    CCDK_LAUNCH_CHECK();
+    unsigned long long* d_range = &ctr->misc[0]; // misc[0..1]
+    if (in.shard_count > 1) {
+        unsigned long long* incl = run_len + k;
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceScan::InclusiveSum(t, b, run_len, incl, static_cast<int64_t>(k), s);
+        });
+        k_shard_range<<<1, 32, 0, s>>>(incl, lo, hi, in.shard_rank, in.shard_count, d_range);
+    } else {
+        k_full_range<<<1, 1, 0, s>>>(lo, hi, d_range);
+    }
+    CCDK_LAUNCH_CHECK();
+    uint32_t* nseg = grow<uint32_t>(c.seg_off, 2 * k);
+    uint32_t* off = nseg + k;
+    k_heavy_count<<<grid_for(k, 256), 256, 0, s>>>(run_end, d_range, k, nseg);
+    cub_call(c, [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, nseg, off, static_cast<int64_t>(k), s);
+    });
+    // segments total <= sum over rows of ceil(k / kSeg); grow on demand below
+    uint64_t seg_cap = std::max<uint64_t>(c.segs.cap / sizeof(Seg), 1024);
+    Seg* segs = grow<Seg>(c.segs, seg_cap);
+
+    // StqStats round sizes
+    if (in.want_rounds) {
+        unsigned long long* hist = grow<unsigned long long>(c.rounds, 2 * (k + 1));
+        CCDK_CUDA_CHECK(cudaMemsetAsync(hist, 0, (k + 1) * sizeof(unsigned long long), s));
+        k_run_hist<<<grid_for(k, 256), 256, 0, s>>>(run_len, k, hist, &ctr->misc[2]);
+        CCDK_LAUNCH_CHECK();
+    }
+
+    // sizes needed on the host: heavy segment count (for the buffer) and max run
+    unsigned long long host_ctr[8];
+    auto read_ctr = [&]() {
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(host_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+    };
+    {
+        // total heavy segments = off[k-1] + nseg[k-1]
+        uint32_t tail[2];
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[0], off + k - 1, 4, cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[1], nseg + k - 1, 4, cudaMemcpyDeviceToHost, s));
+        read_ctr();
+        const uint64_t total = static_cast<uint64_t>(tail[0]) + tail[1];
+        if (total > seg_cap) {
+            seg_cap = total;
+            segs = grow<Seg>(c.segs, seg_cap);
+        }
+    }
+    out.pair_tests = host_ctr[1];
+    if (in.want_rounds) {
+        const uint64_t max_run = host_ctr[4 + 2];
+        c.last_rounds.assign(max_run, 0);
+        if (max_run) {
+            unsigned long long* hist = c.rounds.as<unsigned long long>();
+            unsigned long long* rev = hist + (k + 1);
+            k_reverse<<<grid_for(max_run, 256), 256, 0, s>>>(hist, max_run, max_run, rev);
+            unsigned long long* scan = hist; // reuse: hist no longer needed after reversing
+            cub_call(c, [&](void* t, size_t& b) {
+                return cub::DeviceScan::InclusiveSum(t, b, rev, scan, static_cast<int64_t>(max_run), s);
+            });
+            // scan[i] = sum_{x >= max_run - i} hist[x] = round_sizes[max_run - 1 - i]
+            k_reverse<<<grid_for(max_run, 256), 256, 0, s>>>(scan, max_run, max_run - 1, rev);
+            CCDK_LAUNCH_CHECK();
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(c.last_rounds.data(), rev, max_run * 8,
+                                            cudaMemcpyDeviceToHost, s));
+            CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+    }
+    k_heavy_gen<<<grid_for(k, 256), 256, 0, s>>>(run_end, nseg, off, k, segs, &ctr->n_heavy);
+    CCDK_LAUNCH_CHECK();
+
+    // K5 sweep (re-run once with a larger buffer if the candidate count overflows)
+    const int nb = ceil_log2(k);
+    c.last_nb = nb;
+    if (c.pair_capacity < 8 * k)
+        c.pair_capacity = std::max<uint64_t>(8 * k, uint64_t(1) << 20);
+    uint64_t n_pairs = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        unsigned long long* keys = grow<unsigned long long>(c.pair_keys, c.pair_capacity);
+        CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->n_pairs, 0, 8, s));
+        SweepArgs sa {};
+        sa.smin_a = smin_a;
+        sa.smax_a = smax_a;
+        sa.sbox = sbox;
+        sa.svid = svid;
+        sa.sraw = sraw;
+        sa.run_end = run_end;
+        sa.range = d_range;
+        sa.row0 = lo;
+        sa.k = k;
+        sa.nb = nb;
+        sa.bf = bf;
+        sa.bf_lo = in.range_begin;
+        sa.bf_hi = in.range_end;
+        sa.keys = keys;
+        sa.cap = c.pair_capacity;
+        sa.n_pairs = &ctr->n_pairs;
+        sa.segs = segs;
+        sa.n_heavy = &ctr->n_heavy;
+        if (hi > lo)
+            k_sweep_tile<<<grid_for(hi - lo, kTB), kTB, 0, s>>>(sa);
+        k_sweep_heavy<<<4 * c.num_sms, 256, 0, s>>>(sa);
+        CCDK_LAUNCH_CHECK();
+        read_ctr();
+        n_pairs = host_ctr[0];
+        if (n_pairs <= c.pair_capacity)
+            break;
+        c.pair_capacity = n_pairs + n_pairs / 4;
+    }
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[2], s));
+
+    // K6 canonical order
+    unsigned long long* sorted = grow<unsigned long long>(c.pair_keys_sorted, std::max<uint64_t>(n_pairs, 1));
+    if (n_pairs) {
+        unsigned long long* keys = c.pair_keys.as<unsigned long long>();
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, keys, sorted, static_cast<int64_t>(n_pairs),
+                                                  0, 2 * nb, s);
+        });
+        if (in.unique) {
+            unsigned long long* nsel = &ctr->misc[3];
+            cub_call(c, [&](void* t, size_t& b) {
+                return cub::DeviceSelect::Unique(t, b, sorted, keys, nsel, static_cast<int64_t>(n_pairs), s);
+            });
+            read_ctr();
+            n_pairs = host_ctr[4 + 3];
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(sorted, keys, n_pairs * 8, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    CCDK_CUDA_CHECK(cudaEventRecord(ev[3], s));
+    int axis = 0;
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(&axis, d_axis, sizeof axis, cudaMemcpyDeviceToHost, s));
+    CCDK_CUDA_CHECK(cudaEventSynchronize(ev[3]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_axis_sort, ev[0], ev[1]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_sweep, ev[1], ev[2]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_pairsort, ev[2], ev[3]));
+    for (auto& e : ev)
+        cudaEventDestroy(e);
+    out.axis = axis;
+    out.n_pairs = n_pairs;
+    c.last_n_pairs = n_pairs;
+}
+
+} // namespace ccdk

@@ -1,0 +1,262 @@
+// Internal declarations shared by the ccdk translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ccdk.h"
+
+namespace ccdk {
+
+// ------------------------------------------------------------------ errors
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define CCDK_CUDA_CHECK(expr)                                                          \
+    do {                                                                               \
+        cudaError_t err__ = (expr);                                                    \
+        if (err__ != cudaSuccess) {                                                    \
+            if (err__ == cudaErrorMemoryAllocation)                                    \
+                throw ::ccdk::Error(CCDK_OOM, std::string(#expr) + ": "                \
+                                                  + cudaGetErrorString(err__));        \
+            throw ::ccdk::Error(CCDK_CUDA, std::string(__FILE__) + ":"                 \
+                                               + std::to_string(__LINE__) + " " #expr  \
+                                               ": " + cudaGetErrorString(err__));      \
+        }                                                                              \
+    } while (0)
+
+#define CCDK_LAUNCH_CHECK() CCDK_CUDA_CHECK(cudaGetLastError())
+
+// ------------------------------------------------------------ device memory
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release()
+    {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    // grow-only; contents are not preserved
+    void* ensure(size_t bytes)
+    {
+        if (bytes == 0)
+            bytes = 16;
+        if (bytes > cap) {
+            release();
+            size_t c = bytes + bytes / 4;
+            CCDK_CUDA_CHECK(cudaMalloc(&p, c));
+            cap = c;
+        }
+        return p;
+    }
+    template <typename T>
+    T* as() const
+    {
+        return static_cast<T*>(p);
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~PinnedBuf()
+    {
+        if (p)
+            cudaFreeHost(p);
+    }
+    void* ensure(size_t bytes)
+    {
+        if (bytes > cap) {
+            if (p)
+                cudaFreeHost(p);
+            p = nullptr;
+            CCDK_CUDA_CHECK(cudaMallocHost(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+};
+
+// Device-side scene (canonical slot order V, E, F; aabb.cpp:79-105).
+struct DevScene {
+    DevBuf v0, v1, edges, faces;
+    uint64_t nv = 0, ne = 0, nf = 0;
+    bool valid = false;
+};
+
+// Device work counters, one struct in device memory per context.
+struct DevCounters {
+    unsigned long long n_pairs;       // sweep output cursor
+    unsigned long long pair_tests;    // sum of run lengths in the range
+    unsigned long long n_heavy;       // heavy sweep segments
+    unsigned long long error;         // first error code seen by a kernel
+    unsigned long long misc[4];
+};
+
+// Narrow-phase device scalars.
+struct NarrowScalars {
+    unsigned long long cur_n;       // intervals in the current generation
+    unsigned long long next_n;      // append cursor of the next generation
+    unsigned long long dirty_n;     // queries whose ToI dropped this generation
+    unsigned long long dropped;     // intervals of exhausted queries dropped
+    unsigned long long evaluations;
+    unsigned long long split_actions;
+    unsigned long long peak;        // max compacted queue size
+    unsigned long long gen;         // generation index
+    unsigned long long cont;        // 1 while another generation is needed
+    unsigned long long sem_overflow;
+    unsigned long long phys_overflow;
+    unsigned long long finish_ticket;
+    unsigned long long total_splits;
+    unsigned long long global_toi_bits;
+    unsigned long long any_flags;   // OR of per-query flags
+    unsigned long long vf_count;
+};
+
+struct Ctx;
+
+// -------------------------------------------------------- kernel launchers
+// geometry (ccdk_geometry.cu)
+void launch_round(Ctx& c, const double* x, uint64_t n, float* dn, float* up);
+// build canonical boxes: SoA mins/maxs [3][k], owner vertex triples + rank.
+void launch_build_boxes(Ctx& c, const double* v0, const double* v1, uint64_t nv,
+                        const uint32_t* e, uint64_t ne, const uint32_t* f, uint64_t nf,
+                        double inflation, float* bmin, float* bmax, uint4* vids);
+void launch_soa_to_aos(Ctx& c, const float* bmin, const float* bmax, uint64_t k, float* mn,
+                       float* mx, uint8_t* kind, uint32_t* index, uint64_t nv, uint64_t ne);
+
+// broad phase (ccdk_broad.cu)
+struct BroadOut {
+    uint64_t n_pairs = 0;     // candidates (canonical, unique)
+    uint64_t pair_tests = 0;
+    int axis = 0;
+    float ms_axis_sort = 0, ms_sweep = 0, ms_pairsort = 0;
+};
+// General broad phase over SoA boxes whose slot order is owner order (rank =
+// slot) or, with owner arrays, an arbitrary box list.
+struct BroadIn {
+    const float* bmin = nullptr; // [3][k]
+    const float* bmax = nullptr;
+    const uint4* vids = nullptr; // (v0, v1, v2, rank); absent vertices = 0xffffffff
+    const uint32_t* raw = nullptr; // raw input position per slot (bf ranges); null = identity
+    uint64_t k = 0;
+    int method = CCDK_BROAD_STQ;
+    uint64_t range_begin = 0, range_end = UINT64_MAX;
+    uint32_t shard_rank = 0, shard_count = 1;
+    bool want_rounds = false;
+    bool unique = false; // duplicate owners possible
+};
+void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out);
+
+// narrow phase (ccdk_narrow.cu)
+struct NarrowIn {
+    const uint8_t* kind = nullptr;   // device
+    const double* points = nullptr;  // device, n*24
+    const double* sep = nullptr;     // device or null
+    uint64_t n = 0;
+    ccdk_narrow_cfg cfg {};
+    uint64_t queue_capacity = UINT64_MAX;
+};
+struct NarrowOut {
+    ccdk_narrow_stats stats {};
+    double* toi = nullptr;     // device, n (owned by ctx)
+    uint8_t* flags = nullptr;  // device, n
+};
+void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out);
+void launch_inclusion(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,
+                      uint64_t n, double* out);
+void launch_process(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,
+                    const uint16_t* depth, const double* t_star, const double* sep, uint64_t n,
+                    const ccdk_narrow_cfg& cfg, uint8_t* action, double* cand_t,
+                    uint8_t* zdiag, double* children, uint16_t* child_depth);
+// classify canonical keys (lo<<nb | hi, ranks = slots) into queries
+void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
+                          const double* v0, const double* v1, uint64_t nv,
+                          const uint32_t* e, uint64_t ne, const uint32_t* f, uint8_t* kind,
+                          double* pts);
+void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
+                        const uint8_t* own_kind, const uint32_t* own_index, uint64_t nv,
+                        uint64_t ne, uint64_t* ids);
+
+// ------------------------------------------------------------------ context
+
+struct Ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::mutex mu;
+    uint64_t interval_capacity = 0; // 0 = auto
+
+    DevScene scene;
+
+    // boxes / broad phase
+    DevBuf bmin, bmax, vids, raw;      // slot order
+    DevBuf own_kind, own_index;        // owner of each slot (general mode)
+    DevBuf sort_keys_in, sort_keys_out, sort_vals_in, sort_vals_out;
+    DevBuf smin_a, smax_a, sbox, svid; // sorted SoA
+    DevBuf run_end, seg_off, segs, prefix;
+    DevBuf pair_keys, pair_keys_sorted;
+    DevBuf rounds;
+    DevBuf cub_tmp;
+    DevBuf counters;                   // DevCounters
+    DevBuf axis;                       // int + reduction partials
+    DevBuf partials;
+    uint64_t pair_capacity = 0;
+    int last_nb = 0;                   // bits per rank in the pair keys
+    uint64_t last_n_pairs = 0;
+    std::vector<uint64_t> last_rounds;
+    bool last_pairs_general = false;
+
+    // queries / narrow phase
+    DevBuf q_kind, q_points, q_sep;
+    DevBuf iv_qid[2], iv_t[2], iv_u[2], iv_v[2], iv_dep[2];
+    DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
+    DevBuf nscal;                      // NarrowScalars
+    uint64_t last_query_count = 0;
+
+    // staging for API calls
+    DevBuf tmp[8];
+    PinnedBuf pin;
+
+    // last step results
+    DevBuf last_toi;                   // double
+};
+
+inline dim3 grid_for(uint64_t n, int block)
+{
+    uint64_t g = (n + block - 1) / block;
+    if (g == 0)
+        g = 1;
+    if (g > 0x7fffffffULL)
+        g = 0x7fffffffULL;
+    return dim3(static_cast<unsigned>(g));
+}
+
+inline int ceil_log2(uint64_t k)
+{
+    int b = 1;
+    while ((uint64_t(1) << b) < k)
+        ++b;
+    return b;
+}
+
+} // namespace ccdk

@@ -1,0 +1,276 @@
+// Outward-rounded fp64 interval inclusion of the CCD root function, bit-exact
+// with the reference (proj/include/ccdkit/interval.hpp:16-92 and
+// proj/src/narrowphase.cpp:30-187).
+//
+// Exactness rules: every arithmetic op is an explicit
+// round-to-nearest intrinsic (__dadd_rn/__dsub_rn/__dmul_rn: no FMA
+// contraction whatever the flags), and every result bound moves exactly one
+// representable step outward, with |x| < 1e-250 flushed to +/-1e-250.
+//
+// Two widening policies:
+//   Fast  — nextafter as ONE directed-rounding add: x (+)_ru 2^-1074 is the
+//           successor of x for every finite |x| >= 1e-250 (the exact sum lies
+//           strictly between x and its successor), so up(x) is DADD.RU plus a
+//           |x| < kFlush select.  Equal to the reference's bit increment for
+//           every finite x; differs only for x = -inf (reference: -DBL_MAX).
+//   Exact — the reference's integer bit increment incl. inf/NaN handling.
+// A query whose coordinates all satisfy |x| <= 2^1000 can never produce an
+// infinity inside evaluate_box (|F| <= 18 max|x| + rounding), so Fast is
+// exact for it; the kernels route any other query through Exact.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+namespace ccdk {
+namespace iv {
+
+constexpr double kFlush = 1e-250;                   // interval.hpp:34
+constexpr double kTiny = 4.9406564584124654e-324;   // 2^-1074
+constexpr double kFastLimit = 1.0715086071862673e+301; // 2^1000
+
+struct Fast {
+    static __device__ __forceinline__ double up(double x)
+    {
+        const double r = __dadd_ru(x, kTiny);
+        return fabs(x) < kFlush ? kFlush : r;
+    }
+    static __device__ __forceinline__ double dn(double x)
+    {
+        const double r = __dadd_rd(x, -kTiny);
+        return fabs(x) < kFlush ? -kFlush : r;
+    }
+};
+
+struct Exact {
+    static __device__ __forceinline__ double up(double x)
+    {
+        if (isnan(x) || x == CUDART_INF)
+            return x;
+        if (x < kFlush && x > -kFlush)
+            return kFlush;
+        unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+        b += (b >> 63) ? ~0ull : 1ull; // toward +inf: +1 ulp for x >= 0, -1 for x < 0
+        return __longlong_as_double(static_cast<long long>(b));
+    }
+    static __device__ __forceinline__ double dn(double x) { return -up(-x); }
+};
+
+struct I {
+    double lo, hi;
+};
+
+template <class W>
+__device__ __forceinline__ I add(I a, I b)
+{
+    return { W::dn(__dadd_rn(a.lo, b.lo)), W::up(__dadd_rn(a.hi, b.hi)) };
+}
+
+template <class W>
+__device__ __forceinline__ I sub(I a, I b)
+{
+    return { W::dn(__dsub_rn(a.lo, b.hi)), W::up(__dsub_rn(a.hi, b.lo)) };
+}
+
+// scale_nn (narrowphase.cpp:30-33): exact point factor p in [0, 1].
+template <class W>
+__device__ __forceinline__ I scale(double p, I a)
+{
+    return { W::dn(__dmul_rn(p, a.lo)), W::up(__dmul_rn(p, a.hi)) };
+}
+
+// std::min / std::max semantics (first argument wins ties / NaN)
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+__device__ __forceinline__ double mid2(I a) { return __dmul_rn(0.5, __dadd_rn(a.lo, a.hi)); }
+
+// Width 2^-d of a dyadic domain interval at bisection depth d (d <= 1074).
+__device__ __forceinline__ double dyadic_width(unsigned d)
+{
+    if (d <= 1022)
+        return __longlong_as_double(static_cast<long long>(1023 - d) << 52);
+    return __longlong_as_double(1ll << (1074 - d));
+}
+
+struct Box {
+    double tlo, thi, ulo, uhi, vlo, vhi;
+};
+
+struct Eval {
+    I range[3];
+    double infl[3]; // influences(), narrowphase.cpp:89-107
+};
+
+// evaluate_box (narrowphase.cpp:35-85) + influences (89-107).
+//
+// Same operations and the same operands as the reference, reorganised so the
+// live set stays small: components are independent, so the loop runs
+// component-outer; point deltas are formed once per component (the reference
+// forms the same values once per t-end); u- and v-terms that the reference
+// recomputes per corner are formed once per (t-end, u) and (t-end, v).  All
+// duplicated reference computations are deterministic, so the bits agree.
+// Corner index bits follow the reference: bit0 = t, bit1 = u, bit2 = v.
+// The hull starts from corner 0 like the reference; min/max of the remaining
+// corners is order-independent (bounds are never +/-0 after widening, and a
+// NaN operand is ignored by std::min/max unless it is the running value).
+template <class W>
+__device__ __forceinline__ void evaluate(bool vf, const double* __restrict__ P, const Box& b,
+                                         Eval& ev)
+{
+    ev.infl[0] = ev.infl[1] = ev.infl[2] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double x0[4];
+        I dl[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            x0[p] = __ldg(P + 3 * p + c);
+            const double x1 = __ldg(P + 12 + 3 * p + c);
+            const double d = __dsub_rn(x1, x0[p]); // point(x1) - point(x0): both bounds
+            dl[p] = { W::dn(d), W::up(d) };
+        }
+        double m0[4]; // corner midpoints at t = lo, indexed by (u bit) | (v bit) << 1
+        I rng;
+#pragma unroll
+        for (int tb = 0; tb < 2; ++tb) {
+            const double t = tb ? b.thi : b.tlo;
+            I at[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const I s = scale<W>(t, dl[p]);
+                at[p] = { W::dn(__dadd_rn(x0[p], s.lo)), W::up(__dadd_rn(x0[p], s.hi)) };
+            }
+            // VF: origin 1, u 1->2; EE: origin 2, u 0->1 (selects, not runtime indexing)
+            const I a_org = vf ? at[1] : at[2];
+            const I a_uto = vf ? at[2] : at[1];
+            const I a_ufr = vf ? at[1] : at[0];
+            const I base = sub<W>(at[0], a_org);
+            const I du = sub<W>(a_uto, a_ufr);
+            const I dv = sub<W>(at[3], a_org);
+            I su[2], vt[2];
+#pragma unroll
+            for (int cu = 0; cu < 2; ++cu) {
+                const I ut = scale<W>(cu ? b.uhi : b.ulo, du);
+                su[cu] = vf ? sub<W>(base, ut) : add<W>(base, ut);
+            }
+#pragma unroll
+            for (int cv = 0; cv < 2; ++cv)
+                vt[cv] = scale<W>(cv ? b.vhi : b.vlo, dv);
+            double m[4];
+#pragma unroll
+            for (int uv = 0; uv < 4; ++uv) {
+                const I f = sub<W>(su[uv & 1], vt[uv >> 1]);
+                if (tb == 0 && uv == 0) {
+                    rng = f;
+                } else {
+                    rng.lo = smin(rng.lo, f.lo);
+                    rng.hi = smax(rng.hi, f.hi);
+                }
+                m[uv] = mid2(f);
+            }
+            // u influence: corners differing in bit1; v influence: bit2
+            ev.infl[1] = smax(ev.infl[1], fabs(__dsub_rn(m[1], m[0])));
+            ev.infl[1] = smax(ev.infl[1], fabs(__dsub_rn(m[3], m[2])));
+            ev.infl[2] = smax(ev.infl[2], fabs(__dsub_rn(m[2], m[0])));
+            ev.infl[2] = smax(ev.infl[2], fabs(__dsub_rn(m[3], m[1])));
+            if (tb == 0) {
+#pragma unroll
+                for (int uv = 0; uv < 4; ++uv)
+                    m0[uv] = m[uv];
+            } else {
+#pragma unroll
+                for (int uv = 0; uv < 4; ++uv)
+                    ev.infl[0] = smax(ev.infl[0], fabs(__dsub_rn(m[uv], m0[uv])));
+            }
+        }
+        ev.range[c] = rng;
+    }
+}
+
+// splittable (narrowphase.cpp:109-113)
+__device__ __forceinline__ bool splittable(double lo, double hi)
+{
+    const double mid = __dadd_rn(lo, __dmul_rn(0.5, __dsub_rn(hi, lo)));
+    return mid > lo && mid < hi;
+}
+
+struct Cfg {
+    double delta, t_max;
+    int no_zero_toi;
+};
+
+enum : int { kPruned = 0, kCollision = 1, kSplit = 2 };
+
+// process_interval (narrowphase.cpp:134-187).  Returns the action; for Split
+// `dim` is the bisection dimension (0 t, 1 u, 2 v).
+template <class W>
+__device__ __forceinline__ int process_one(bool vf, const double* __restrict__ P, const Box& b,
+                                           double t_star, double d, const Cfg& cfg,
+                                           double& cand_t, bool& zdiag, int& dim,
+                                           bool& evaluated)
+{
+    zdiag = false;
+    evaluated = false;
+    dim = -1;
+    if (b.tlo >= t_star || b.tlo >= cfg.t_max)
+        return kPruned;
+    if (vf && __dadd_rn(b.ulo, b.vlo) > 1.0)
+        return kPruned;
+    Eval ev;
+    evaluate<W>(vf, P, b, ev);
+    evaluated = true;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        if (ev.range[c].lo > d || ev.range[c].hi < -d)
+            return kPruned;
+    const bool force_zero = cfg.no_zero_toi && b.tlo == 0.0;
+    if (!force_zero) {
+        bool inside = true;
+        double wmax = __dsub_rn(ev.range[0].hi, ev.range[0].lo);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            inside = inside && ev.range[c].lo >= -d && ev.range[c].hi <= d;
+            wmax = smax(wmax, __dsub_rn(ev.range[c].hi, ev.range[c].lo));
+        }
+        if (wmax < cfg.delta || inside) {
+            cand_t = b.tlo;
+            return kCollision;
+        }
+    }
+    // first splittable dimension with strictly larger influence (t < u < v
+    // on ties); written without runtime array indexing to stay in registers
+    double best = 0.0;
+    if (splittable(b.tlo, b.thi)) {
+        dim = 0;
+        best = ev.infl[0];
+    }
+    if (splittable(b.ulo, b.uhi) && (dim < 0 || ev.infl[1] > best)) {
+        dim = 1;
+        best = ev.infl[1];
+    }
+    if (splittable(b.vlo, b.vhi) && (dim < 0 || ev.infl[2] > best))
+        dim = 2;
+    if (dim < 0) {
+        cand_t = b.tlo;
+        zdiag = force_zero;
+        return kCollision;
+    }
+    return kSplit;
+}
+
+// A query takes the Fast widening when every coordinate is <= 2^1000 in
+// magnitude (see the header comment).
+__device__ __forceinline__ bool fast_ok(const double* __restrict__ P)
+{
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 24; ++i)
+        ok = ok && fabs(__ldg(P + i)) <= kFastLimit; // NaN compares false -> Exact
+    return ok;
+}
+
+} // namespace iv
+} // namespace ccdk

@@ -1,0 +1,622 @@
+// K7 classify, K8 breadth-first interval narrow phase, K9 reduction.
+//
+// Reference: proj/src/narrowphase.cpp:189-311 (narrow_phase) and
+// proj/src/broadphase.cpp:194-239 (classify).
+//
+// K8 keeps the reference's schedule semantics exactly (SURVEY §7 "hard
+// parts"): whole generations; pruning against a per-query ToI SNAPSHOT taken
+// at the generation start (a dirty list refreshes only queries whose ToI
+// dropped); per-query split budget counted per generation (an atomic request
+// counter: the first max_splits requests are admitted, any later one folds
+// its t.lo and marks the query exhausted, and the exhausted query's admitted
+// children are folded and dropped at the start of the next generation).  All
+// of these are order-independent, so unordered atomic appends reproduce the
+// reference's serial fold bit for bit.
+//
+// Interval records are compact SoA: query id, (t,u,v).lo as doubles and the
+// three bisection depths packed in a u64; hi = lo + 2^-depth exactly.
+#include <cub/cub.cuh>
+
+#include "ccdk_internal.cuh"
+#include "ccdk_interval.cuh"
+
+namespace ccdk {
+
+namespace {
+
+constexpr unsigned kNoGen = 0xffffffffu;
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+constexpr int kGenBlock = 128;
+
+struct GenArgs {
+    const uint8_t* kind;
+    const double* pts;
+    const double* sep;
+    double sep_default;
+    iv::Cfg cfg;
+    unsigned long long max_splits;
+    unsigned long long* toi;
+    unsigned long long* snap;
+    unsigned long long* splits;
+    unsigned* exh_gen;
+    uint8_t* zdiag;
+    unsigned* dirty;
+    unsigned* dirty_mark;
+    uint32_t* qid[2];
+    double* t[2];
+    double* u[2];
+    double* v[2];
+    unsigned long long* dep[2];
+    unsigned long long phys_cap;
+    unsigned long long sem_cap;
+    NarrowScalars* sc;
+};
+
+__device__ __forceinline__ unsigned long long dbits(double x)
+{
+    return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
+__device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned v)
+{
+    const unsigned s = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && s)
+        atomicAdd(dst, static_cast<unsigned long long>(s));
+}
+
+// One BFS generation: process_interval on every live interval + the fold.
+__global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
+{
+    NarrowScalars* sc = a.sc;
+    if (!sc->cont)
+        return;
+    const unsigned long long n = sc->cur_n;
+    const unsigned gen = static_cast<unsigned>(sc->gen);
+    const int cb = gen & 1, nb = cb ^ 1;
+    const uint32_t* __restrict__ qid = a.qid[cb];
+    const double* __restrict__ ts = a.t[cb];
+    const double* __restrict__ us = a.u[cb];
+    const double* __restrict__ vs = a.v[cb];
+    const unsigned long long* __restrict__ ds = a.dep[cb];
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    unsigned evals = 0, split_actions = 0, dropped = 0;
+
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x
+             + (threadIdx.x & ~31u);
+         base < n; base += stride) {
+        const unsigned long long i = base + lane;
+        bool admit = false;
+        unsigned q = 0;
+        double tlo = 0, ulo = 0, vlo = 0;
+        unsigned long long dp = 0;
+        int dim = -1;
+        if (i < n) {
+            q = qid[i];
+            tlo = ts[i];
+            ulo = us[i];
+            vlo = vs[i];
+            dp = ds[i];
+            const unsigned dt = dp & 0xffff, du = (dp >> 16) & 0xffff, dv = (dp >> 32) & 0xffff;
+            if (a.exh_gen[q] < gen) {
+                // exhausted in an earlier generation: fold t.lo and drop
+                // (narrowphase.cpp:280-291)
+                atomicMin(&a.toi[q], dbits(tlo));
+                if (a.cfg.no_zero_toi && tlo == 0.0)
+                    a.zdiag[q] = 1;
+                ++dropped;
+            } else {
+                iv::Box b;
+                b.tlo = tlo;
+                b.thi = __dadd_rn(tlo, iv::dyadic_width(dt));
+                b.ulo = ulo;
+                b.uhi = __dadd_rn(ulo, iv::dyadic_width(du));
+                b.vlo = vlo;
+                b.vhi = __dadd_rn(vlo, iv::dyadic_width(dv));
+                const double t_star = __longlong_as_double(static_cast<long long>(a.snap[q]));
+                const double d = a.sep ? a.sep[q] : a.sep_default;
+                const bool vf = a.kind[q] == CCDK_QUERY_VF;
+                const double* P = a.pts + 24ull * q;
+                double cand = 0;
+                bool zd = false, evald = false;
+                int act;
+                if (iv::fast_ok(P))
+                    act = iv::process_one<iv::Fast>(vf, P, b, t_star, d, a.cfg, cand, zd, dim, evald);
+                else
+                    act = iv::process_one<iv::Exact>(vf, P, b, t_star, d, a.cfg, cand, zd, dim, evald);
+                evals += evald;
+                if (act == iv::kCollision) {
+                    const unsigned long long cb2 = dbits(cand);
+                    const unsigned long long old = atomicMin(&a.toi[q], cb2);
+                    if (cb2 < old && atomicExch(&a.dirty_mark[q], gen + 1) != gen + 1)
+                        a.dirty[atomicAdd(&sc->dirty_n, 1ull)] = q;
+                    if (zd)
+                        a.zdiag[q] = 1;
+                } else if (act == iv::kSplit) {
+                    ++split_actions;
+                    const bool exempt = a.cfg.no_zero_toi && tlo == 0.0;
+                    if (exempt || atomicAdd(&a.splits[q], 1ull) < a.max_splits) {
+                        admit = true;
+                    } else {
+                        // budget exhausted (narrowphase.cpp:263-271)
+                        atomicMin(&a.toi[q], dbits(tlo));
+                        a.exh_gen[q] = gen;
+                        if (a.cfg.no_zero_toi && tlo == 0.0)
+                            a.zdiag[q] = 1;
+                    }
+                }
+            }
+        }
+        // warp-aggregated append of the two children per admitted split
+        const unsigned mask = __ballot_sync(0xffffffffu, admit);
+        if (mask) {
+            unsigned long long slot0 = 0;
+            const int leader = __ffs(mask) - 1;
+            if (lane == static_cast<unsigned>(leader))
+                slot0 = atomicAdd(&sc->next_n, 2ull * __popc(mask));
+            slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+            if (admit) {
+                const unsigned long long s = slot0 + 2ull * __popc(mask & ((1u << lane) - 1));
+                if (s + 2 <= a.phys_cap) {
+                    const unsigned dd = (dp >> (16 * dim)) & 0xffff;
+                    const double lo = dim == 0 ? tlo : dim == 1 ? ulo : vlo;
+                    // split_box (narrowphase.cpp:122-132): exact midpoint
+                    const double mid = __dadd_rn(lo, __dmul_rn(0.5, iv::dyadic_width(dd)));
+                    const unsigned long long dpc = dp + (1ull << (16 * dim));
+                    a.qid[nb][s] = q;
+                    a.qid[nb][s + 1] = q;
+                    a.t[nb][s] = tlo;
+                    a.t[nb][s + 1] = dim == 0 ? mid : tlo;
+                    a.u[nb][s] = ulo;
+                    a.u[nb][s + 1] = dim == 1 ? mid : ulo;
+                    a.v[nb][s] = vlo;
+                    a.v[nb][s + 1] = dim == 2 ? mid : vlo;
+                    a.dep[nb][s] = dpc;
+                    a.dep[nb][s + 1] = dpc;
+                } else {
+                    sc->phys_overflow = 1;
+                }
+            }
+        }
+    }
+    warp_add(&sc->evaluations, evals);
+    warp_add(&sc->split_actions, split_actions);
+    warp_add(&sc->dropped, dropped);
+}
+
+// Generation end: refresh snapshots of queries whose ToI dropped, then (last
+// block) the queue bookkeeping of narrowphase.cpp:299-304.
+__global__ void k_finish(GenArgs a)
+{
+    NarrowScalars* sc = a.sc;
+    if (!sc->cont)
+        return;
+    const unsigned long long nd = sc->dirty_n;
+    for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < nd;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const unsigned q = a.dirty[i];
+        a.snap[q] = a.toi[q];
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&sc->finish_ticket, 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0)
+        return;
+    __threadfence();
+    const unsigned long long compacted = sc->cur_n - sc->dropped;
+    if (compacted > sc->peak)
+        sc->peak = compacted;
+    if (compacted > a.sem_cap)
+        sc->sem_overflow = 1;
+    const unsigned long long raw_next = sc->next_n;
+    if (raw_next > a.phys_cap)
+        sc->phys_overflow = 1;
+    sc->gen += 1;
+    sc->cur_n = raw_next > a.phys_cap ? a.phys_cap : raw_next;
+    sc->next_n = 0;
+    sc->dirty_n = 0;
+    sc->dropped = 0;
+    sc->finish_ticket = 0;
+    sc->cont = (raw_next > 0 && !sc->sem_overflow && !sc->phys_overflow) ? 1 : 0;
+    __threadfence();
+}
+
+__global__ void k_init_queries(unsigned long long n, unsigned long long* toi,
+                               unsigned long long* snap, unsigned long long* splits,
+                               unsigned* exh_gen, uint8_t* zdiag, unsigned* dirty_mark,
+                               uint32_t* qid, double* t, double* u, double* v,
+                               unsigned long long* dep)
+{
+    for (unsigned long long q = blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        toi[q] = kInfBits;
+        snap[q] = kInfBits;
+        splits[q] = 0;
+        exh_gen[q] = kNoGen;
+        zdiag[q] = 0;
+        dirty_mark[q] = 0;
+        qid[q] = static_cast<uint32_t>(q); // one root box [0,1]^3 per query
+        t[q] = 0.0;
+        u[q] = 0.0;
+        v[q] = 0.0;
+        dep[q] = 0;
+    }
+}
+
+// Per-query outputs and the K9 reductions (global min ToI, total_splits).
+__global__ void k_outputs(unsigned long long n, const unsigned long long* toi,
+                          const unsigned long long* splits, const unsigned* exh_gen,
+                          const uint8_t* zdiag, unsigned long long max_splits,
+                          NarrowScalars* sc, double* toi_out, uint8_t* flags_out)
+{
+    const bool overflow = sc->sem_overflow != 0;
+    unsigned long long mn = kInfBits, tot = 0;
+    unsigned fl = 0;
+    for (unsigned long long q = blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const unsigned long long tb = overflow ? kInfBits : toi[q];
+        toi_out[q] = __longlong_as_double(static_cast<long long>(tb));
+        const uint8_t f = overflow ? 0
+                                   : static_cast<uint8_t>((exh_gen[q] != kNoGen ? CCDK_FLAG_TOLERANCE_HIT : 0u)
+                                                          | (zdiag[q] ? CCDK_FLAG_ZERO_TOI_DIAG : 0u));
+        flags_out[q] = f;
+        fl |= f;
+        mn = tb < mn ? tb : mn;
+        const unsigned long long s = splits[q];
+        tot += s < max_splits ? s : max_splits;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_down_sync(0xffffffffu, mn, o);
+        mn = other < mn ? other : mn;
+        tot += __shfl_down_sync(0xffffffffu, tot, o);
+    }
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&sc->global_toi_bits, mn);
+        if (fl)
+            atomicOr(&sc->any_flags, static_cast<unsigned long long>(fl));
+        if (tot)
+            atomicAdd(&sc->total_splits, tot);
+    }
+}
+
+// ---- single-interval API kernels (inclusion_box / process_interval)
+
+__global__ void k_inclusion(const uint8_t* kind, const double* pts, const double* boxes,
+                            unsigned long long n, double* out)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= n)
+        return;
+    const double* P = pts + 24 * i;
+    const double* bx = boxes + 6 * i;
+    const iv::Box b { bx[0], bx[1], bx[2], bx[3], bx[4], bx[5] };
+    iv::Eval ev;
+    const bool vf = kind[i] == CCDK_QUERY_VF;
+    if (iv::fast_ok(P))
+        iv::evaluate<iv::Fast>(vf, P, b, ev);
+    else
+        iv::evaluate<iv::Exact>(vf, P, b, ev);
+    for (int c = 0; c < 3; ++c) {
+        out[6 * i + 2 * c] = ev.range[c].lo;
+        out[6 * i + 2 * c + 1] = ev.range[c].hi;
+    }
+}
+
+__global__ void k_process(const uint8_t* kind, const double* pts, const double* boxes,
+                          const uint16_t* depth, const double* t_star, const double* sep,
+                          unsigned long long n, iv::Cfg cfg, double sep_default,
+                          uint8_t* action, double* cand_t, uint8_t* zdiag, double* children,
+                          uint16_t* child_depth)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= n)
+        return;
+    const double* P = pts + 24 * i;
+    const double* bx = boxes + 6 * i;
+    const iv::Box b { bx[0], bx[1], bx[2], bx[3], bx[4], bx[5] };
+    const double d = (sep && sep[i] >= 0.0) ? sep[i] : sep_default;
+    const bool vf = kind[i] == CCDK_QUERY_VF;
+    double cand = CUDART_INF;
+    bool zd = false, evald = false;
+    int dim = -1;
+    const int act = iv::fast_ok(P)
+        ? iv::process_one<iv::Fast>(vf, P, b, t_star[i], d, cfg, cand, zd, dim, evald)
+        : iv::process_one<iv::Exact>(vf, P, b, t_star[i], d, cfg, cand, zd, dim, evald);
+    action[i] = static_cast<uint8_t>(act);
+    cand_t[i] = act == iv::kCollision ? cand : CUDART_INF;
+    zdiag[i] = zd;
+    // children default to a default-constructed IntervalBox ([0,1]^3, depth 0)
+    double ch[12] = { 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1 };
+    uint16_t cd[6] = { 0, 0, 0, 0, 0, 0 };
+    if (act == iv::kSplit) {
+        for (int s = 0; s < 2; ++s)
+            for (int j = 0; j < 6; ++j)
+                ch[6 * s + j] = bx[j];
+        const double lo = bx[2 * dim], hi = bx[2 * dim + 1];
+        const double mid = __dadd_rn(lo, __dmul_rn(0.5, __dsub_rn(hi, lo)));
+        ch[2 * dim + 1] = mid;     // left.hi
+        ch[6 + 2 * dim] = mid;     // right.lo
+        for (int s = 0; s < 2; ++s)
+            for (int j = 0; j < 3; ++j)
+                cd[3 * s + j] = depth[3 * i + j] + (j == dim ? 1 : 0);
+    }
+    for (int j = 0; j < 12; ++j)
+        children[12 * i + j] = ch[j];
+    for (int j = 0; j < 6; ++j)
+        child_depth[6 * i + j] = cd[j];
+}
+
+// ---- K7: candidate keys -> narrow queries (broadphase.cpp:194-239).
+// Canonical keys list every VF pair (left = vertex) before every EE pair
+// (left = edge), which is the pipeline's VF-then-EE order
+// (pipeline.cpp:162-165); all pairs already passed keep_pair in the sweep.
+__global__ void k_classify_keys(const unsigned long long* keys, unsigned long long n, int nb,
+                                const double* __restrict__ v0, const double* __restrict__ v1,
+                                unsigned long long nv, const uint32_t* __restrict__ e,
+                                unsigned long long ne, const uint32_t* __restrict__ f,
+                                uint8_t* kind, double* pts)
+{
+    const unsigned long long q = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (q >= n)
+        return;
+    const unsigned long long key = keys[q];
+    const unsigned long long lo = key >> nb;
+    const unsigned long long hi = key & ((1ull << nb) - 1);
+    uint32_t pv[4];
+    if (lo < nv) { // vertex-face: (p, t0, t1, t2)
+        const unsigned long long fi = hi - nv - ne;
+        pv[0] = static_cast<uint32_t>(lo);
+        pv[1] = f[3 * fi];
+        pv[2] = f[3 * fi + 1];
+        pv[3] = f[3 * fi + 2];
+        kind[q] = CCDK_QUERY_VF;
+    } else { // edge-edge: (e0a, e0b, e1a, e1b)
+        const unsigned long long ea = lo - nv, eb = hi - nv;
+        pv[0] = e[2 * ea];
+        pv[1] = e[2 * ea + 1];
+        pv[2] = e[2 * eb];
+        pv[3] = e[2 * eb + 1];
+        kind[q] = CCDK_QUERY_EE;
+    }
+    double* out = pts + 24 * q;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            out[3 * p + c] = v0[3ull * pv[p] + c];
+            out[12 + 3 * p + c] = v1[3ull * pv[p] + c];
+        }
+}
+
+__global__ void k_keys_to_ids(const unsigned long long* keys, unsigned long long n, int nb,
+                              const uint8_t* own_kind, const uint32_t* own_index,
+                              unsigned long long nv, unsigned long long ne,
+                              unsigned long long* ids)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= n)
+        return;
+    const unsigned long long key = keys[i];
+    const unsigned long long r[2] = { key >> nb, key & ((1ull << nb) - 1) };
+    for (int s = 0; s < 2; ++s) {
+        unsigned long long id;
+        if (own_kind) {
+            id = (static_cast<unsigned long long>(own_kind[r[s]]) << 32) | own_index[r[s]];
+        } else {
+            const unsigned long long x = r[s];
+            id = x < nv ? x : x < nv + ne ? ((1ull << 32) | (x - nv)) : ((2ull << 32) | (x - nv - ne));
+        }
+        ids[2 * i + s] = id;
+    }
+}
+
+template <typename T>
+T* grow(DevBuf& b, uint64_t n)
+{
+    return static_cast<T*>(b.ensure(n * sizeof(T)));
+}
+
+// One device run over queries [0, n) of `in`; returns false on physical
+// interval-buffer overflow (caller halves).
+bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const double* pts,
+              const double* sep, double* toi_out, uint8_t* flags_out, ccdk_narrow_stats& st)
+{
+    cudaStream_t s = c.stream;
+    uint64_t cap = c.interval_capacity;
+    if (cap == 0) {
+        size_t free_b = 0, total_b = 0;
+        CCDK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t by_mem = static_cast<uint64_t>(free_b / 2) / 72;
+        cap = std::max<uint64_t>(4 * n, uint64_t(1) << 24);
+        cap = std::min<uint64_t>(cap, by_mem);
+        cap = std::max<uint64_t>(cap, n);
+    }
+    if (cap < n)
+        return false;
+    GenArgs a {};
+    a.kind = kind;
+    a.pts = pts;
+    a.sep = sep;
+    a.sep_default = in.cfg.min_separation;
+    a.cfg = { in.cfg.delta, in.cfg.t_max, in.cfg.no_zero_toi };
+    a.max_splits = in.cfg.max_splits;
+    a.toi = grow<unsigned long long>(c.toi_live, n);
+    a.snap = grow<unsigned long long>(c.toi_snap, n);
+    a.splits = grow<unsigned long long>(c.splits, n);
+    a.exh_gen = grow<unsigned>(c.exh_gen, n);
+    a.zdiag = grow<uint8_t>(c.zdiag, n);
+    a.dirty = grow<unsigned>(c.dirty, 2 * n);
+    a.dirty_mark = a.dirty + n;
+    for (int b = 0; b < 2; ++b) {
+        a.qid[b] = grow<uint32_t>(c.iv_qid[b], cap);
+        a.t[b] = grow<double>(c.iv_t[b], cap);
+        a.u[b] = grow<double>(c.iv_u[b], cap);
+        a.v[b] = grow<double>(c.iv_v[b], cap);
+        a.dep[b] = grow<unsigned long long>(c.iv_dep[b], cap);
+    }
+    a.phys_cap = cap;
+    a.sem_cap = in.queue_capacity;
+    a.sc = static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars)));
+
+    NarrowScalars init {};
+    init.cur_n = n;
+    init.cont = 1;
+    init.global_toi_bits = kInfBits;
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    const dim3 ig = grid_for(n, 256);
+    k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(
+        n, a.toi, a.snap, a.splits, a.exh_gen, a.zdiag, a.dirty_mark, a.qid[0], a.t[0], a.u[0],
+        a.v[0], a.dep[0]);
+    CCDK_LAUNCH_CHECK();
+
+    int blocks_per_sm = 0;
+    CCDK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_generation,
+                                                                  kGenBlock, 0));
+    const unsigned gen_grid = static_cast<unsigned>(std::max(1, blocks_per_sm) * c.num_sms);
+    const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
+
+    NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
+    const int batch = 8;
+    for (;;) {
+        for (int g = 0; g < batch; ++g) {
+            k_generation<<<gen_grid, kGenBlock, 0, s>>>(a);
+            k_finish<<<fin_grid, 256, 0, s>>>(a);
+        }
+        CCDK_LAUNCH_CHECK();
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars),
+                                        cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (!host_sc->cont)
+            break;
+    }
+    if (host_sc->phys_overflow)
+        return false;
+    k_outputs<<<std::min<unsigned>(ig.x, 4096u), 256, 0, s>>>(n, a.toi, a.splits, a.exh_gen,
+                                                              a.zdiag, a.max_splits, a.sc,
+                                                              toi_out, flags_out);
+    CCDK_LAUNCH_CHECK();
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
+    CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+    st.overflow = host_sc->sem_overflow ? 1 : 0;
+    const double g = __builtin_bit_cast(double, static_cast<uint64_t>(host_sc->global_toi_bits));
+    st.global_toi = st.overflow ? INFINITY : std::min(st.global_toi, g);
+    st.peak_queue = std::max<uint64_t>(st.peak_queue, std::max<uint64_t>(host_sc->peak, n));
+    st.total_splits += host_sc->total_splits;
+    st.evaluations += host_sc->evaluations;
+    st.split_actions += host_sc->split_actions;
+    st.generations = std::max<uint64_t>(st.generations, host_sc->gen);
+    return true;
+}
+
+void run_range(Ctx& c, const NarrowIn& in, uint64_t lo, uint64_t hi, double* toi_out,
+               uint8_t* flags_out, ccdk_narrow_stats& st)
+{
+    const uint64_t n = hi - lo;
+    if (n == 0)
+        return;
+    if (run_once(c, in, n, in.kind + lo, in.points + 24 * lo, in.sep ? in.sep + lo : nullptr,
+                 toi_out + lo, flags_out + lo, st))
+        return;
+    if (n <= 1)
+        throw Error(CCDK_CAPACITY, "narrow phase: interval buffer cannot hold one query's frontier");
+    const uint64_t mid = lo + n / 2;
+    run_range(c, in, lo, mid, toi_out, flags_out, st);
+    run_range(c, in, mid, hi, toi_out, flags_out, st);
+}
+
+} // namespace
+
+void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
+{
+    ccdk_narrow_stats st {};
+    st.global_toi = INFINITY;
+    const uint64_t n = in.n;
+    out.toi = grow<double>(c.out_toi, n);
+    out.flags = grow<uint8_t>(c.out_flags, n);
+    cudaEvent_t e0, e1;
+    CCDK_CUDA_CHECK(cudaEventCreate(&e0));
+    CCDK_CUDA_CHECK(cudaEventCreate(&e1));
+    CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+    if (n > 0 && n > in.queue_capacity) {
+        // narrowphase.cpp:215-218: seeds alone exceed the capacity
+        st.overflow = 1;
+        st.peak_queue = 0;
+        CCDK_CUDA_CHECK(cudaMemsetAsync(out.flags, 0, n, c.stream));
+        const dim3 g = grid_for(n, 256);
+        NarrowScalars* sc = static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars)));
+        NarrowScalars init {};
+        init.sem_overflow = 1;
+        init.global_toi_bits = kInfBits;
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(sc, &init, sizeof init, cudaMemcpyHostToDevice, c.stream));
+        unsigned long long* dummy = grow<unsigned long long>(c.toi_live, n);
+        k_outputs<<<std::min<unsigned>(g.x, 4096u), 256, 0, c.stream>>>(
+            n, dummy, dummy, grow<unsigned>(c.exh_gen, n), grow<uint8_t>(c.zdiag, n), 0, sc,
+            out.toi, out.flags);
+        CCDK_LAUNCH_CHECK();
+    } else if (n > 0) {
+        run_range(c, in, 0, n, out.toi, out.flags, st);
+    }
+    CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
+    CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    st.device_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (st.overflow) {
+        st.global_toi = INFINITY;
+    }
+    out.stats = st;
+}
+
+void launch_inclusion(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,
+                      uint64_t n, double* out)
+{
+    if (!n)
+        return;
+    k_inclusion<<<grid_for(n, 128), 128, 0, c.stream>>>(kind, pts, boxes, n, out);
+    CCDK_LAUNCH_CHECK();
+}
+
+void launch_process(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,
+                    const uint16_t* depth, const double* t_star, const double* sep, uint64_t n,
+                    const ccdk_narrow_cfg& cfg, uint8_t* action, double* cand_t, uint8_t* zdiag,
+                    double* children, uint16_t* child_depth)
+{
+    if (!n)
+        return;
+    const iv::Cfg ic { cfg.delta, cfg.t_max, cfg.no_zero_toi };
+    k_process<<<grid_for(n, 128), 128, 0, c.stream>>>(kind, pts, boxes, depth, t_star, sep, n, ic,
+                                                      cfg.min_separation, action, cand_t, zdiag,
+                                                      children, child_depth);
+    CCDK_LAUNCH_CHECK();
+}
+
+void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb, const double* v0,
+                          const double* v1, uint64_t nv, const uint32_t* e, uint64_t ne,
+                          const uint32_t* f, uint8_t* kind, double* pts)
+{
+    if (!n)
+        return;
+    k_classify_keys<<<grid_for(n, 128), 128, 0, c.stream>>>(
+        reinterpret_cast<const unsigned long long*>(keys), n, nb, v0, v1, nv, e, ne, f, kind, pts);
+    CCDK_LAUNCH_CHECK();
+}
+
+void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb, const uint8_t* own_kind,
+                        const uint32_t* own_index, uint64_t nv, uint64_t ne, uint64_t* ids)
+{
+    if (!n)
+        return;
+    k_keys_to_ids<<<grid_for(n, 256), 256, 0, c.stream>>>(
+        reinterpret_cast<const unsigned long long*>(keys), n, nb, own_kind, own_index, nv, ne,
+        reinterpret_cast<unsigned long long*>(ids));
+    CCDK_LAUNCH_CHECK();
+}
+
+} // namespace ccdk

@@ -1,0 +1,344 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU checkers.
+
+The checkers are the reference itself (oracle/_ref, bit-exact target) and our
+C restatement (oracle/liborc.so).  Bars (SURVEY §8 / BASELINE.md §4):
+  * boxes, rounding, candidate sets, round sizes: bit-exact;
+  * inclusion boxes, process_interval, per-query ToI and flags, total_splits,
+    peak_queue: bit-exact (stronger than the north star's "ToI within delta,
+    zero false negatives", which bit-exactness implies).
+"""
+import numpy as np
+import pytest
+
+from paper_2112_06300_b200 import abi, ccdkit as ck, scenes
+from paper_2112_06300_b200.ccdkit import NarrowConfig, PipelineConfig, SweepRange
+
+from fixtures import (concat, plane_crossing_query, plane_crossing_scene, random_boxes,
+                      random_subboxes, random_triangle_soup, special_doubles)
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def assert_bits(a, b):
+    assert a.shape == b.shape
+    np.testing.assert_array_equal(bits(a), bits(b))
+
+
+# ------------------------------------------------------------------ geometry
+
+def test_rounding_matches_reference(ctx, orc):
+    x = special_doubles(7, 20000)
+    dn, up = ck.round_reduced(x, ctx)
+    edn, eup = orc.round_reduced(x)
+    assert_bits(dn, edn)
+    assert_bits(up, eup)
+    assert ck.round_down_reduced(0.1, ctx).view(np.uint32) == 0x3DCCCCCC
+    assert ck.round_up_reduced(0.1, ctx).view(np.uint32) == 0x3DCCCCCD
+
+
+def test_rounding_rejects_non_finite(ctx):
+    with pytest.raises(ck.InvalidInput):
+        ck.round_reduced(np.array([1.0, np.nan]), ctx)
+    with pytest.raises(ck.InvalidInput):
+        ck.round_reduced(np.array([np.inf]), ctx)
+
+
+@pytest.mark.parametrize("inflation", [0.0, 0.01, 0.5])
+def test_build_boxes_bit_exact(ctx, ref, inflation):
+    for s in [scenes.make_cloth_scene(20, 17, 0.02, 1.0, 3), scenes.make_box_soup(50, 6.0, 0.4, 0.9, 11),
+              random_triangle_soup(5, 3000)]:
+        got = ck.build_boxes(s, inflation, ctx=ctx)
+        exp = ref.build_boxes(s, inflation)
+        for g, e in zip(got.as_tuple(), exp):
+            np.testing.assert_array_equal(np.asarray(g).view(np.uint8), np.asarray(e).view(np.uint8))
+
+
+def test_build_boxes_known_answers(ctx):
+    s = scenes.SceneStep([[0, 0, 0]], [[0, 0, 0]], np.zeros((0, 2)), np.zeros((0, 3)))
+    b = ck.build_boxes(s, ctx=ctx)
+    assert b.min_corner.tolist() == [[0, 0, 0]] and b.max_corner.tolist() == [[0, 0, 0]]
+    s = scenes.SceneStep([[0, 0, 0], [1, 0, 0]], [[0, 0, 1], [1, 0, 1]], [[0, 1]], np.zeros((0, 3)))
+    b = ck.build_boxes(s, ctx=ctx)
+    assert len(b) == 3 and b.owner_kind[2] == ck.KIND_EDGE and b.owner_index[2] == 0
+    assert b.min_corner[2].tolist() == [0, 0, 0] and b.max_corner[2].tolist() == [1, 0, 1]
+    b = ck.build_boxes(scenes.SceneStep([[1, 2, 3]], [[1, 2, 3]], np.zeros((0, 2)), np.zeros((0, 3))), 0.1, ctx=ctx)
+    assert (b.max_corner[0].astype(np.float64) - b.min_corner[0] >= 2e-12).all()
+
+
+def test_scene_validation_errors(ctx):
+    good = plane_crossing_scene()
+    bad = scenes.SceneStep(good.vertices_t0, good.vertices_t1, [[0, 7]], good.faces)
+    with pytest.raises(ck.InvalidInput):
+        ck.build_boxes(bad, ctx=ctx)
+    bad = scenes.SceneStep(good.vertices_t0, good.vertices_t1, [[1, 1]], good.faces)
+    with pytest.raises(ck.InvalidInput):
+        ck.build_boxes(bad, ctx=ctx)
+    v = good.vertices_t0.copy()
+    v[0, 0] = np.nan
+    with pytest.raises(ck.InvalidInput):
+        ck.ccd(scenes.SceneStep(v, good.vertices_t1, good.edges, good.faces), ctx=ctx)
+    with pytest.raises(ck.ConfigError):
+        ck.ccd(good, PipelineConfig(narrow=NarrowConfig(delta=0.0)), ctx=ctx)
+
+
+# -------------------------------------------------------------- broad phase
+
+def test_choose_axis(ctx, ref):
+    b, _ = random_boxes(21, 1000, (1, 1, 100))
+    assert ck.choose_axis(b, ctx) == 2 == ref.choose_axis(b.min_corner, b.max_corner)
+    with pytest.raises(ck.InvalidInput):
+        ck.choose_axis(ck.Boxes(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32),
+                                np.zeros(0, np.uint8), np.zeros(0, np.uint32)), ctx)
+    for seed in range(5):
+        b, _ = random_boxes(100 + seed, 3000, (1.0, 1.3, 0.7))
+        assert ck.choose_axis(b, ctx) == ref.choose_axis(b.min_corner, b.max_corner)
+
+
+def test_stq_trivial(ctx):
+    b, s = random_boxes(22, 2)
+    b.min_corner[:] = [[0, 0, 0], [1, 1, 5]]
+    b.max_corner[:] = [[2, 2, 1], [3, 3, 6]]
+    assert ck.stq(b, s, ctx=ctx).shape == (0, 2)
+    b.min_corner[1] = b.min_corner[0]
+    b.max_corner[1] = b.max_corner[0]
+    b.owner_kind[:] = [0, 2]
+    b.owner_index[:] = [0, 0]
+    pairs = ck.stq(b, s, ctx=ctx)
+    assert pairs.tolist() == [[0, 2 << 32]]
+
+
+@pytest.mark.parametrize("method", [abi.BROAD_STQ, abi.BROAD_SAP, abi.BROAD_BF])
+def test_broad_phase_random_sets_bit_exact(ctx, ref, method):
+    rng = scenes.Rng(25)
+    for trial in range(40):
+        n = 1 + int(rng.u64(1)[0] % np.uint64(600))
+        b, s = random_boxes(1000 + trial, n)
+        got = ck._broad(method, b, s, None, None, ctx)
+        exp, _, _ = ref.broad(method, b.as_tuple(), s)
+        np.testing.assert_array_equal(got, exp)
+
+
+def test_stq_stats_and_ranges(ctx, ref):
+    for trial in range(6):
+        b, s = random_boxes(2000 + trial, 300 + 150 * trial)
+        st = ck.StqStats()
+        got = ck.stq(b, s, stats=st, ctx=ctx)
+        exp, rounds, mq = ref.broad(abi.BROAD_STQ, b.as_tuple(), s)
+        np.testing.assert_array_equal(got, exp)
+        assert st.round_sizes == rounds.tolist() and st.max_queue == mq
+        k = len(b)
+        for lo, hi in [(0, k // 3), (k // 3, k), (5, 17), (k - 1, k + 5)]:
+            st = ck.StqStats()
+            got = ck.stq(b, s, stats=st, range=SweepRange(lo, hi), ctx=ctx)
+            exp, rounds, mq = ref.broad(abi.BROAD_STQ, b.as_tuple(), s, lo, hi)
+            np.testing.assert_array_equal(got, exp)
+            assert st.round_sizes == rounds.tolist()
+            got = ck.bf(b, s, range=SweepRange(lo, hi), ctx=ctx)
+            exp, _, _ = ref.broad(abi.BROAD_BF, b.as_tuple(), s, lo, hi)
+            np.testing.assert_array_equal(got, exp)
+
+
+def test_broad_phase_on_scenes(ctx, ref):
+    for s in [scenes.make_cloth_scene(40, 40, 0.02, 1.0, 1), scenes.make_box_soup(300, 8.0, 0.45, 0.9, 42),
+              scenes.config_scene("C3", 0.01)]:
+        b = ck.build_boxes(s, 0.01, ctx=ctx)
+        st = ck.StqStats()
+        got = ck.stq(b, s, stats=st, ctx=ctx)
+        exp, rounds, mq = ref.broad(abi.BROAD_STQ, b.as_tuple(), s)
+        np.testing.assert_array_equal(got, exp)
+        assert st.round_sizes == rounds.tolist()
+
+
+def test_classify_matches_reference(ctx, ref):
+    s = scenes.make_box_soup(60, 5.0, 0.4, 1.0, 9)
+    b = ck.build_boxes(s, 0.01, ctx=ctx)
+    pairs = ck.stq(b, s, ctx=ctx)
+    # add pairs the filter must drop: shared vertex, wrong kinds, reversed
+    extra = np.array([[ck.pack_id(1, 0), ck.pack_id(1, 1)], [ck.pack_id(0, 0), ck.pack_id(0, 5)],
+                      [ck.pack_id(2, 3), ck.pack_id(0, 0)], [ck.pack_id(0, 0), ck.pack_id(2, 0)]],
+                     np.uint64)
+    allp = np.concatenate([pairs, extra, pairs[::7]])
+    got = ck.classify(allp, s, ctx=ctx)
+    ek, ep, es, envf = ref.classify(allp, s)
+    assert got.n_vf == envf
+    np.testing.assert_array_equal(got.queries.kind, ek)
+    assert_bits(got.queries.points, ep)
+    np.testing.assert_array_equal(got.sources, es)
+    bad = np.array([[ck.pack_id(0, 0), ck.pack_id(2, 99999)]], np.uint64)
+    with pytest.raises(ck.InvalidInput):
+        ck.classify(bad, s, ctx=ctx)
+
+
+# -------------------------------------------------------------- narrow phase
+
+def test_inclusion_box_bits(ctx, ref):
+    q = plane_crossing_query()
+    r = ck.inclusion_box(0, q.points[0], ctx=ctx)
+    assert r[4] == -float.fromhex("0x1.0000000000008p+0") and r[5] == float.fromhex("0x1.0000000000004p+0")
+    assert r[0] == -float.fromhex("0x1.8000000000008p-1") and r[1] == float.fromhex("0x1.0000000000004p-2")
+    qb = scenes.random_queries(500, seed=31)
+    boxes, _ = random_subboxes(31, 500)
+    got = ck.inclusion_boxes(qb.kind, qb.points, boxes, ctx)
+    exp = np.stack([ref.inclusion_box(qb.kind[i], qb.points[i], boxes[i]) for i in range(500)])
+    assert_bits(got, exp)
+
+
+def test_inclusion_box_extreme_magnitudes(ctx, ref):
+    """Queries beyond 2^1000 take the bit-increment (Exact) widening path."""
+    qb = scenes.random_queries(64, seed=77)
+    pts = qb.points * np.where(np.arange(64)[:, None] % 2 == 0, 1e307, 1e-300)
+    boxes, _ = random_subboxes(78, 64)
+    got = ck.inclusion_boxes(qb.kind, pts, boxes, ctx)
+    exp = np.stack([ref.inclusion_box(qb.kind[i], pts[i], boxes[i]) for i in range(64)])
+    assert_bits(got, exp)
+
+
+def test_process_interval_matches_reference(ctx, ref):
+    n = 400
+    qb = concat(scenes.random_queries(n - 1, seed=41), plane_crossing_query())
+    boxes, depth = random_subboxes(42, n)
+    rng = scenes.Rng(43)
+    t_star = np.where(rng.doubles(n) < 0.3, rng.doubles(n), np.inf)
+    for cfg in [NarrowConfig(), NarrowConfig(delta=0.3, min_separation=0.01, no_zero_toi=True),
+                NarrowConfig(t_max=0.4)]:
+        a, ct, zd, ch, cd = ck.process_intervals(qb.kind, qb.points, boxes, depth, t_star, cfg, ctx=ctx)
+        for i in range(n):
+            ea, ect, ezd, ech, ecd = ref.process_interval(qb.kind[i], qb.points[i], boxes[i], depth[i],
+                                                          t_star[i], -1.0, cfg.to_c())
+            assert a[i] == ea and zd[i] == ezd, i
+            assert bits(np.array([ct[i]]))[0] == bits(np.array([ect]))[0]
+            assert_bits(ch[i], ech)
+            np.testing.assert_array_equal(cd[i], ecd)
+
+
+def test_plane_crossing_known_answers(ctx):
+    q = plane_crossing_query()
+    out = ck.narrow_phase(q, ctx=ctx)
+    assert out.toi[0] == 0.5 - 2.0 ** -21 and out.total_splits == 449 and out.peak_queue == 16
+    out = ck.narrow_phase(q, NarrowConfig(min_separation=0.25), ctx=ctx)
+    assert out.global_toi == 0.37451171875
+    out = ck.narrow_phase(q, NarrowConfig(max_splits=4), ctx=ctx)
+    assert out.toi[0] == 0.25 and out.flags[0] & abi.FLAG_TOLERANCE_HIT
+    out = ck.narrow_phase(concat(q, q, q), queue_capacity=2, ctx=ctx)
+    assert out.overflow and np.isinf(out.global_toi)
+    empty = ck.narrow_phase(scenes.QueryBatch(np.zeros(0, np.uint8), np.zeros((0, 24))), ctx=ctx)
+    assert np.isinf(empty.global_toi) and empty.toi.size == 0
+
+
+def _narrow_equal(got, toi, flags, st):
+    assert_bits(got.toi, toi)
+    np.testing.assert_array_equal(got.flags, flags)
+    assert got.overflow == bool(st.overflow)
+    if not got.overflow:
+        assert got.total_splits == st.total_splits
+        assert got.peak_queue == st.peak_queue
+        assert bits(np.array([got.global_toi]))[0] == bits(np.array([st.global_toi]))[0]
+
+
+@pytest.mark.parametrize("max_splits", [1 << 20, 37, 8, 1])
+def test_narrow_phase_random_bit_exact(ctx, ref, max_splits):
+    qb = scenes.random_queries(3000, seed=1003)
+    cfg = NarrowConfig(max_splits=max_splits)
+    got = ck.narrow_phase(qb, cfg, ctx=ctx)
+    _narrow_equal(got, *ref.narrow_phase(qb.kind, qb.points, cfg.to_c()))
+
+
+def test_narrow_phase_separations_and_no_zero(ctx, ref):
+    qb = scenes.random_queries(1500, seed=34)
+    seps = np.abs(scenes.Rng(35).doubles(1500)) * 0.05
+    for cfg, sp in [(NarrowConfig(min_separation=0.02), None), (NarrowConfig(), seps),
+                    (NarrowConfig(no_zero_toi=True), None), (NarrowConfig(no_zero_toi=True, max_splits=50), seps),
+                    (NarrowConfig(t_max=0.3, delta=1e-4), None)]:
+        got = ck.narrow_phase(qb, cfg, per_query_min_sep=sp, ctx=ctx)
+        _narrow_equal(got, *ref.narrow_phase(qb.kind, qb.points, cfg.to_c(), seps=sp))
+
+
+def test_narrow_phase_degenerate_families(ctx, ref):
+    qb = scenes.degenerate_queries(64, seed=5)
+    cfg = NarrowConfig(max_splits=20000)
+    got = ck.narrow_phase(qb, cfg, ctx=ctx)
+    _narrow_equal(got, *ref.narrow_phase(qb.kind, qb.points, cfg.to_c()))
+
+
+def test_narrow_phase_capacity_semantics(ctx, ref):
+    qb = scenes.random_queries(200, seed=8)
+    for cap in [150, 300, 5000]:
+        got = ck.narrow_phase(qb, NarrowConfig(), queue_capacity=cap, ctx=ctx)
+        toi, flags, st = ref.narrow_phase(qb.kind, qb.points, NarrowConfig().to_c(), capacity=cap)
+        assert got.overflow == bool(st.overflow), cap
+        if not st.overflow:
+            _narrow_equal(got, toi, flags, st)
+
+
+def test_narrow_phase_physical_halving(ctx, ref):
+    """A tiny device interval buffer forces the batch-halving path; per-query
+    results stay bit-exact (each query's result depends only on itself)."""
+    qb = scenes.random_queries(400, seed=9)
+    ctx.set_interval_capacity(512)
+    try:
+        got = ck.narrow_phase(qb, ctx=ctx)
+    finally:
+        ctx.set_interval_capacity(0)
+    toi, flags, st = ref.narrow_phase(qb.kind, qb.points, NarrowConfig().to_c())
+    assert_bits(got.toi, toi)
+    np.testing.assert_array_equal(got.flags, flags)
+    assert got.total_splits == st.total_splits
+
+
+# ------------------------------------------------------------------ pipeline
+
+@pytest.mark.parametrize("name", ["cloth30", "soup", "C1", "C2", "C3", "C4"])
+def test_ccd_matches_reference(ctx, ref, name):
+    s = {"cloth30": lambda: scenes.make_cloth_scene(30, 30, 0.02, 1.0, 1),
+         "soup": lambda: scenes.make_box_soup(40, 5.0, 0.4, 1.0, 1005),
+         "C1": lambda: scenes.config_scene("C1", 0.05),
+         "C2": lambda: scenes.config_scene("C2", 0.01),
+         "C3": lambda: scenes.config_scene("C3", 0.004),
+         "C4": lambda: scenes.config_scene("C4", 0.004)}[name]()
+    cfg = PipelineConfig(inflation=0.01)
+    got = ck.ccd(s, cfg, ctx=ctx)
+    exp, pairs = ref.ccd(s, cfg.to_c())
+    np.testing.assert_array_equal(got.candidates, pairs)
+    assert got.candidate_count == exp.candidate_count and got.query_count == exp.query_count
+    assert bits(np.array([got.toi.toi]))[0] == bits(np.array([exp.toi]))[0]
+    assert got.toi.tolerance_hit == bool(exp.tolerance_hit)
+    assert got.tracked_peak_bytes == exp.tracked_peak_bytes
+    assert set(got.per_stage_times) == {"CB", "BP", "SO/CD", "NP"}
+
+
+def test_ccd_trivial_scenes(ctx):
+    s = scenes.SceneStep([[0, 0, 0], [1, 0, 0], [0, 1, 0], [50, 0, 0], [51, 0, 0], [50, 1, 0]],
+                         [[0, 0, 0], [1, 0, 0], [0, 1, 0], [50, 0, 0], [51, 0, 0], [50, 1, 0]],
+                         [[0, 1], [0, 2], [1, 2], [3, 4], [3, 5], [4, 5]], [[0, 1, 2], [3, 4, 5]])
+    r = ck.ccd(s, ctx=ctx)
+    assert not r.toi.collision() and r.candidate_count == 0 and r.batch_count == 1
+    r = ck.ccd(plane_crossing_scene(), ctx=ctx)
+    assert 0.5 - 2.0 ** -20 <= r.toi.toi <= 0.5 and r.candidate_count >= 1
+    empty = scenes.SceneStep(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 2)), np.zeros((0, 3)))
+    assert not ck.ccd(empty, ctx=ctx).toi.collision()
+
+
+def test_resident_step_shards_union(ctx, ref):
+    s = scenes.make_cloth_scene(60, 60, 0.02, 1.0, 4)
+    cfg = PipelineConfig(inflation=0.01)
+    rs = ck.ResidentScene(s, ctx)
+    full = rs.step(cfg)
+    full_pairs = rs.candidates(full.candidate_count)
+    for shards in [2, 3, 8]:
+        parts, tois = [], []
+        for r in range(shards):
+            rep = rs.step(cfg, r, shards)
+            parts.append(rs.candidates(rep.candidate_count))
+            tois.append(rep.toi.toi)
+        union = np.concatenate(parts)
+        union = union[np.lexsort((union[:, 1], union[:, 0]))]
+        np.testing.assert_array_equal(union, full_pairs)
+        assert min(tois) == full.toi.toi
+    # determinism across repeated device runs
+    again = rs.step(cfg)
+    assert again.toi.toi == full.toi.toi and again.candidate_count == full.candidate_count
