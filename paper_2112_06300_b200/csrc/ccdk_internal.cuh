@@ -5,6 +5,8 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -36,7 +38,31 @@ void set_last_error(const std::string& msg);
         }                                                                              \
     } while (0)
 
-#define CCDK_LAUNCH_CHECK() CCDK_CUDA_CHECK(cudaGetLastError())
+#define CCDK_LAUNCH_CHECK()                                                             \
+    do {                                                                                \
+        CCDK_CUDA_CHECK(cudaGetLastError());                                            \
+        if (::ccdk::debug_enabled()) {                                                  \
+            cudaError_t e__ = cudaDeviceSynchronize();                                  \
+            std::fprintf(stderr, "[ccdk] %s:%d %s\n", __FILE__, __LINE__,               \
+                         cudaGetErrorString(e__));                                      \
+            CCDK_CUDA_CHECK(e__);                                                       \
+        }                                                                               \
+    } while (0)
+
+inline bool debug_enabled()
+{
+    static const bool d = std::getenv("CCDK_DEBUG") != nullptr;
+    return d;
+}
+
+// Debug tracing (CCDK_DEBUG=1): synchronise and report each stage.
+#define CCDK_TRACE(c, msg)                                                              \
+    do {                                                                                \
+        if (::ccdk::debug_enabled()) {                                                  \
+            cudaError_t e__ = cudaStreamSynchronize((c).stream);                        \
+            std::fprintf(stderr, "[ccdk] %s: %s\n", msg, cudaGetErrorString(e__));      \
+        }                                                                               \
+    } while (0)
 
 // ------------------------------------------------------------ device memory
 

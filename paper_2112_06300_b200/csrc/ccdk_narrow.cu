@@ -482,6 +482,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
 
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
     const int batch = 8;
+    static const bool debug = getenv("CCDK_DEBUG") != nullptr;
     for (;;) {
         for (int g = 0; g < batch; ++g) {
             k_generation<<<gen_grid, kGenBlock, 0, s>>>(a);
@@ -491,8 +492,17 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars),
                                         cudaMemcpyDeviceToHost, s));
         CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (debug)
+            fprintf(stderr, "[ccdk narrow] n=%llu gen=%llu cur=%llu peak=%llu evals=%llu splits=%llu cont=%llu phys=%llu sem=%llu\n",
+                    (unsigned long long)n, host_sc->gen, host_sc->cur_n, host_sc->peak,
+                    host_sc->evaluations, host_sc->split_actions, host_sc->cont,
+                    host_sc->phys_overflow, host_sc->sem_overflow);
         if (!host_sc->cont)
             break;
+        // a BFS tree is at most 3 x 1075 bisections deep; more generations
+        // than that means corrupted state, never a legitimate run
+        if (host_sc->gen > 4000)
+            throw Error(CCDK_CUDA, "narrow phase: generation limit exceeded (internal error)");
     }
     if (host_sc->phys_overflow)
         return false;

@@ -36,7 +36,7 @@ class CapacityError(CcdkError):
 
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()  # default_context() -> Context() -> lib() re-enters
 
 _SIGS = {
     "ccdk_abi_version": (C.c_int, []),
