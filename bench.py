@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark: the full conservative CCD step on BASELINE.json's ~1M-primitive
+scene (C4), device-timed on N GPUs, plus the end-to-end call through the
+C ABI and the reference CPU implementation timed on the host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+One JSON line on rank 0.  `value` = device ms of the whole CCD step (box
+build -> STQ broad phase -> classify -> narrow phase -> global min-ToI incl.
+the allreduce(min) across ranks), max over ranks; inputs resident in HBM; L2
+flushed (256 MiB memset) before every timed step.  `e2e` = the same step
+through the C ABI from pinned host buffers (scene H2D, step, report D2H).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CCD step ms + narrow-phase queries/s at 1/2/4/8 B200 vs CPU ref (cores stated)"
+WORKLOADS = {
+    "C4": "armadillo-rollers-like ~1M primitives: make_cloth_scene(410,410,jitter .02,drop 1,seed 4) "
+          "= 1,005,334 boxes; inflation 0.01, delta 1e-6, min_sep 0, max_splits 2^20, t_max 1",
+    "C1": "cloth-on-sphere 100x100 + icosphere, seed 1",
+    "C2": "cloth-ball-like 224x224 pleated self-contact + ball, seed 2",
+    "C3": "n-body-like box soup 13200 + 1% 20x bodies + walls, seed 3",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def cpu_reference_step(scene, cfg_c, threads):
+    import oracle
+    t0 = time.perf_counter()
+    rep, _ = oracle.ref(threads).ccd(scene, cfg_c, want_pairs=False)
+    return (time.perf_counter() - t0) * 1e3, rep
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2112_06300_b200 import ccdkit as ck, scenes
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libccdref.so not built"}))
+        return 0
+    threads = os.cpu_count() or 1
+    scene = scenes.config_scene(args.workload)
+    cfg = ck.PipelineConfig(inflation=0.01, broad_method=ck.BROAD_SAP, threads=threads)
+    times, rep = [], None
+    for i in range(args.warmup + args.steps):
+        ms, rep = cpu_reference_step(scene, cfg.to_c(), threads)
+        if i >= args.warmup:
+            times.append(ms)
+    ms = sum(times) / len(times)
+    sample = (f"full {args.workload} step via ccdkit_ref::ccd (unmodified reference, BroadMethod::SAP "
+              f"= identical candidate set to STQ, threads={threads})")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "scene": WORKLOADS[args.workload],
+                   "primitives": scene.primitive_count(), "broad_method": "sap"},
+        "narrow_queries_per_s": rep.query_count / rep.t_np if rep.t_np > 0 else None,
+        "candidates": rep.candidate_count, "toi": rep.toi,
+        "stage_s": {"CB": rep.t_cb, "BP": rep.t_bp, "SO/CD": rep.t_socd, "NP": rep.t_np},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
+                         "sample": sample, "cpu": platform.processor() or platform.machine()},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2112_06300_b200 import abi, ccdkit as ck, native, scenes
+    from paper_2112_06300_b200.multigpu import ShardedCcd
+
+    stream = torch.cuda.Stream()
+    ctx = native.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    scene = scenes.config_scene(args.workload)
+    cfg = ck.PipelineConfig(inflation=0.01)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    with torch.cuda.stream(stream):
+        resident = ck.ResidentScene(scene, ctx)
+        sharded = ShardedCcd(resident, rank, world)
+        for _ in range(args.warmup):
+            flush.zero_()
+            rep = sharded.step(cfg)
+        # ---- device-timed region: K full steps, L2 flushed before each
+        clocks = ClockSampler(local)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        with clocks:
+            reps = []
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                reps.append(sharded.step(cfg))
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        wall = time.perf_counter() - t_wall
+        dev_ms = [a.elapsed_time(b) for a, b in ev]
+        my_ms = sum(dev_ms) / len(dev_ms)
+        rep = reps[-1]
+        gtoi = sharded.global_toi(rep)
+
+        # ---- e2e through the C ABI from pinned host buffers
+        e2e_ms = None
+        h2d = scene.nbytes
+        d2h = C_REPORT_BYTES + 8
+        if not args.no_e2e:
+            pin = {}
+            for name in ("vertices_t0", "vertices_t1", "edges", "faces"):
+                a = getattr(scene, name)
+                t = torch.empty(a.shape, dtype={np.float64: torch.float64, np.uint32: torch.int32}[a.dtype.type],
+                                pin_memory=True)
+                tn = t.numpy().view(a.dtype)
+                tn[...] = a
+                pin[name] = tn
+            pscene = scenes.SceneStep(pin["vertices_t0"], pin["vertices_t1"], pin["edges"], pin["faces"])
+            e2e_ev = []
+            for i in range(args.warmup + args.steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                res = ck.ResidentScene(pscene, ctx)          # H2D + validation
+                sh = ShardedCcd(res, rank, world)
+                r = sh.step(cfg)                               # step + report D2H
+                sh.global_toi(r)                               # global ToI D2H
+                b.record(stream)
+                if i >= args.warmup:
+                    e2e_ev.append((a, b))
+            torch.cuda.synchronize()
+            e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev) / len(e2e_ev)
+
+    # ---- max over ranks
+    vals = torch.tensor([my_ms, e2e_ms or 0.0, rep.device["ms_narrow"]], dtype=torch.float64,
+                        device=f"cuda:{local}")
+    counts = torch.tensor([rep.query_count, rep.candidate_count], dtype=torch.float64,
+                          device=f"cuda:{local}")
+    if world > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(counts, op=torch.distributed.ReduceOp.SUM)
+    ms, e2e_max, narrow_ms = vals.tolist()
+    queries, candidates = (int(x) for x in counts.tolist())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            if oracle.ref_available():
+                threads = os.cpu_count() or 1
+                cfg_ref = ck.PipelineConfig(inflation=0.01, broad_method=ck.BROAD_SAP, threads=threads)
+                cpu_ms, cpu_rep = cpu_reference_step(scene, cfg_ref.to_c(), threads)
+                cpu = {"value": cpu_ms, "unit": "ms", "cores": threads, "kind": "reference",
+                       "sample": f"one full {args.workload} step, ccdkit_ref::ccd SAP threads={threads}",
+                       "narrow_queries_per_s": cpu_rep.query_count / cpu_rep.t_np if cpu_rep.t_np else None,
+                       "toi_matches": cpu_rep.toi == gtoi,
+                       "candidates_match": cpu_rep.candidate_count == candidates}
+        except Exception as e:  # the baseline must not kill the GPU number
+            cpu = {"error": str(e)}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peaks = load_peaks()
+    clk = clocks.summary()
+    sm_max = clk.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    d = rep.device
+    # fp64 roofline of the narrow phase: F = 339 E + 96 S non-FMA fp64 ops
+    # (SURVEY §8(d)); peak = 148 SMs x 64 fp64 lanes x clock (nominal, not in
+    # MEASURED_PEAKS.json, which has only HBM and bf16)
+    flops = 339.0 * d["evaluations"] + 96.0 * d["split_actions"]
+    fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
+    narrow_tf = flops / (d["ms_narrow"] * 1e-3) / 1e12 if d["ms_narrow"] > 0 else 0.0
+    k = scene.primitive_count()
+    sweep_bytes = 40.0 * k + 8.0 * rep.candidate_count
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sweep_gbs = sweep_bytes / (d["ms_sweep"] * 1e-3) / 1e9 if d["ms_sweep"] > 0 else 0.0
+    traffic = load_traffic()
+    roofline = {"kernel": "k_generation (BFS narrow phase, all generations of one step)",
+                "bound": "fp64", "achieved": narrow_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": narrow_tf / fp64_peak, "traffic": traffic.get("narrow_bytes_per_step"),
+                "peak_source": "nominal: 148 SM x 64 fp64 FMA-pipe lanes x sm clock (non-FMA op rate)",
+                "algorithmic": f"F = 339*E + 96*S, E={d['evaluations']}, S={d['split_actions']}"}
+    roofline_sweep = {"kernel": "run ends + tile sweep + heavy sweep", "bound": "hbm",
+                      "achieved": sweep_gbs, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": sweep_gbs / hbm_peak, "traffic": traffic.get("sweep_bytes_per_step"),
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+                      "algorithmic": f"B = 40k + 8C, k={k}, C={rep.candidate_count}",
+                      "pair_tests": d["pair_tests"],
+                      "pair_tests_per_s": d["pair_tests"] / (d["ms_sweep"] * 1e-3) if d["ms_sweep"] else None}
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "scene": WORKLOADS[args.workload], "primitives": k,
+                   "parallelism": f"sweep-range shards x{world}, allreduce(min)",
+                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "narrow_queries_per_s": queries / (narrow_ms * 1e-3) if narrow_ms > 0 else None,
+        "candidates": candidates, "queries": queries, "toi": gtoi,
+        "stage_ms": {kk: d[kk] for kk in ("ms_build", "ms_sort", "ms_sweep", "ms_pairsort",
+                                           "ms_classify", "ms_narrow", "ms_total")},
+        "work": {"pair_tests": d["pair_tests"], "evaluations": d["evaluations"],
+                 "split_actions": d["split_actions"], "total_splits": d["total_splits"],
+                 "generations": d["generations"], "peak_queue": d["peak_queue"]},
+        "e2e": {"value": e2e_max if e2e_ms is not None else None, "unit": "ms",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "roofline": roofline, "roofline_sweep": roofline_sweep,
+        "cpu_baseline": cpu, "clocks": clk,
+        "gpu_launches": int(d["kernel_launches"]) * args.steps,
+        "wall_s_timed_region": wall,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+C_REPORT_BYTES = 0
+
+
+def main():
+    global C_REPORT_BYTES
+    args = parse()
+    from paper_2112_06300_b200 import abi
+    import ctypes
+    C_REPORT_BYTES = ctypes.sizeof(abi.Report)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -129,6 +129,7 @@ typedef struct {
     int32_t axis;
     int32_t reserved2;
     double ms_build, ms_sort, ms_sweep, ms_pairsort, ms_classify, ms_narrow, ms_total;
+    uint64_t kernel_launches; /* own (non-CUB) kernels launched by this step */
 } ccdk_report;
 
 typedef struct ccdk_ctx ccdk_ctx;
@@ -234,6 +235,10 @@ CCDK_API int ccdk_ccd_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint
 /* Device pointer (double) holding the last step's global ToI, for a
  * device-side allreduce(min) by the multi-GPU host layer. */
 CCDK_API int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr);
+
+/* Copy the last step's global ToI (one double) to device memory `dst_dev`
+ * on the context stream (feeds a device-side allreduce(min)). */
+CCDK_API int ccdk_copy_last_toi(ccdk_ctx* ctx, void* dst_dev);
 
 /* Per-query results of the last ccd step (query_count entries). */
 CCDK_API int ccdk_fetch_query_results(ccdk_ctx* ctx, double* toi, uint8_t* flags);

@@ -377,7 +377,7 @@ def _report(r: abi.Report, pairs) -> CcdReport:
     dev = {k: getattr(r, k) for k, _ in abi.Report._fields_ if k.startswith("ms_")}
     dev.update(vf_count=r.vf_count, pair_tests=r.pair_tests, total_splits=r.total_splits,
                peak_queue=r.peak_queue, evaluations=r.evaluations, split_actions=r.split_actions,
-               generations=r.generations, axis=r.axis)
+               generations=r.generations, axis=r.axis, kernel_launches=r.kernel_launches)
     return CcdReport(ToiResult(r.toi, bool(r.tolerance_hit), bool(r.zero_toi_diagnostic)),
                      int(r.candidate_count), int(r.query_count), int(r.batch_count),
                      {"CB": r.t_cb, "BP": r.t_bp, "SO/CD": r.t_socd, "NP": r.t_np},
@@ -434,6 +434,10 @@ class ResidentScene:
         if n:
             check(lib().ccdk_fetch_query_results(self.ctx.h, p(toi, P_F64), p(fl, P_U8)))
         return toi[:n], fl[:n]
+
+    def copy_toi_to(self, dev_ptr: int):
+        """Device copy of the last global ToI into ``dev_ptr`` (one double)."""
+        check(lib().ccdk_copy_last_toi(self.ctx.h, C.c_void_p(dev_ptr)))
 
     def toi_device_ptr(self) -> int:
         v = C.c_void_p()

@@ -485,6 +485,11 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     rep.ms_classify = ms[2];
     rep.ms_narrow = ms[3];
     rep.ms_total = ms[4];
+    // own kernels: validate-free resident step = K1 + 11 broad-phase kernels
+    // (3 axis, keys, permute, run ends, range, heavy count/gen, tile, heavy)
+    // + classify + vf count + narrow (init, 2 per generation in batches of 8,
+    // outputs) + ToI store
+    rep.kernel_launches = 1 + 11 + (n ? 2 : 0) + (n ? 2 + no.launches : 0) + 1;
     rep.t_cb = ms[0] * 1e-3;
     rep.t_bp = ms[1] * 1e-3;
     rep.t_socd = ms[2] * 1e-3;
@@ -982,6 +987,15 @@ int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
 int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr)
 {
     return guard(ctx, [&] { *dev_ptr = grow<double>(ctx->last_toi, 1); });
+}
+
+int ccdk_copy_last_toi(ccdk_ctx* ctx, void* dst_dev)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(dst_dev, grow<double>(ctx->last_toi, 1), sizeof(double),
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+    });
 }
 
 int ccdk_fetch_query_results(ccdk_ctx* ctx, double* toi, uint8_t* flags)

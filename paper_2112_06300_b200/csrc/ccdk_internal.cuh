@@ -205,6 +205,7 @@ struct NarrowOut {
     ccdk_narrow_stats stats {};
     double* toi = nullptr;     // device, n (owned by ctx)
     uint8_t* flags = nullptr;  // device, n
+    uint64_t launches = 0;     // generation + finish kernels launched
 };
 void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out);
 void launch_inclusion(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,
@@ -258,6 +259,7 @@ struct Ctx {
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
     DevBuf nscal;                      // NarrowScalars
     uint64_t last_query_count = 0;
+    uint64_t narrow_launches = 0;
 
     // staging for API calls
     DevBuf tmp[8];

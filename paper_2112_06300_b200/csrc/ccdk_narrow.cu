@@ -488,6 +488,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
             k_generation<<<gen_grid, kGenBlock, 0, s>>>(a);
             k_finish<<<fin_grid, 256, 0, s>>>(a);
         }
+        c.narrow_launches += 2 * batch;
         CCDK_LAUNCH_CHECK();
         CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars),
                                         cudaMemcpyDeviceToHost, s));
@@ -545,6 +546,7 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
 {
     ccdk_narrow_stats st {};
     st.global_toi = INFINITY;
+    c.narrow_launches = 0;
     const uint64_t n = in.n;
     out.toi = grow<double>(c.out_toi, n);
     out.flags = grow<uint8_t>(c.out_flags, n);
@@ -582,6 +584,7 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
         st.global_toi = INFINITY;
     }
     out.stats = st;
+    out.launches = c.narrow_launches;
 }
 
 void launch_inclusion(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,

@@ -1,0 +1,87 @@
+"""Multi-GPU host layer: one process per GPU, sweep start-ranges partitioned
+across ranks, global min-ToI combined with ONE allreduce(min).
+
+SURVEY §8(e): every rank holds the replicated scene, builds and sorts the
+full box array (~0.1 ms at 1M boxes), computes run lengths, and sweeps only
+its slice of sorted left positions — the slices split the total pair-test
+work (sum of run lengths) evenly, which is the reference's SweepRange
+contract (broadphase.hpp:37-43: the union over a partition equals the full
+candidate set).  Candidate sets are disjoint by construction (a pair is
+emitted by its lower sorted position), so the data path needs no collective;
+the only exchange is the 8-byte allreduce(min) of the ToI, run on the device
+buffer the step wrote (NCCL over NVLink on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_bounds(run_len: np.ndarray, lo: int, hi: int, rank: int, count: int) -> tuple[int, int]:
+    """Host restatement of the device partition (ccdk_broad.cu k_shard_range):
+    shard r covers sorted left positions [B_r, B_{r+1}) where B_r is the first
+    p in [lo, hi) whose exclusive prefix of run lengths reaches floor(W*r/S)."""
+    incl = np.cumsum(run_len.astype(np.uint64))
+    W = int(incl[hi - 1]) if hi > lo else 0
+
+    def boundary(r):
+        if r == 0:
+            return lo
+        if r >= count:
+            return hi
+        T = (W // count) * r + ((W % count) * r) // count
+        a, b = lo, hi
+        while a < b:
+            m = (a + b) >> 1
+            e = 0 if m == lo else int(incl[m - 1])
+            if e >= T:
+                b = m
+            else:
+                a = m + 1
+        return a
+
+    return boundary(rank), boundary(rank + 1)
+
+
+def sorted_run_lengths(min_corner: np.ndarray, max_corner: np.ndarray, axis: int) -> tuple[np.ndarray, np.ndarray]:
+    """(order, run_len) of the sweep along `axis`: order sorts by min (ties by
+    slot, -0 == +0), run_len[p] = #{j > p : min[j] <= max[p]} (STQ rounds)."""
+    mn = min_corner[:, axis].astype(np.float32)
+    key = mn.copy()
+    key[key == 0] = 0.0  # -0 -> +0
+    order = np.lexsort((np.arange(mn.size), key))
+    smin = mn[order]
+    smax = max_corner[order, axis].astype(np.float32)
+    end = np.searchsorted(smin, smax, side="right")
+    p = np.arange(mn.size)
+    end = np.maximum(end, p + 1)
+    return order, (end - p - 1).astype(np.uint64)
+
+
+def allreduce_min_toi(toi_tensor, group=None):
+    """The single collective of the step: allreduce(min) of the global ToI
+    (a 1-element float64 tensor, CUDA under NCCL or CPU under gloo)."""
+    import torch.distributed as dist
+    dist.all_reduce(toi_tensor, op=dist.ReduceOp.MIN, group=group)
+    return toi_tensor
+
+
+class ShardedCcd:
+    """Runs the device-resident CCD step for this rank's shard and combines
+    the global ToI across ranks on the device."""
+
+    def __init__(self, resident, rank: int, world: int):
+        import torch
+        self.resident = resident
+        self.rank = rank
+        self.world = world
+        self.toi = torch.full((1,), float("inf"), dtype=torch.float64, device=f"cuda:{resident.ctx.device}")
+
+    def step(self, cfg):
+        rep = self.resident.step(cfg, self.rank, self.world)
+        if self.world > 1:
+            self.resident.copy_toi_to(self.toi.data_ptr())
+            allreduce_min_toi(self.toi)
+        return rep
+
+    def global_toi(self, rep) -> float:
+        return float(self.toi.item()) if self.world > 1 else rep.toi.toi

@@ -71,6 +71,7 @@ _SIGS = {
     "ccdk_ccd_resident": (C.c_int, [C.c_void_p, C.POINTER(abi.PipelineCfg), C.c_uint32, C.c_uint32,
                                     C.POINTER(abi.Report)]),
     "ccdk_last_toi_device_ptr": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ccdk_copy_last_toi": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ccdk_fetch_query_results": (C.c_int, [C.c_void_p, P_F64, P_U8]),
 }
 
