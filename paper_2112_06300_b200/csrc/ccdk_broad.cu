@@ -32,7 +32,7 @@ namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kTB = 128;        // left rows per sweep CTA
-constexpr int kTile = 256;      // staged boxes per tile
+constexpr int kTile = 512;      // staged boxes per tile (8 KiB of float4)
 constexpr uint32_t kCap = 4096; // per-row window handled by the tile kernel
 constexpr uint32_t kSeg = 2048; // heavy-row segment length
 constexpr int kRedBlocks = 256;
@@ -347,8 +347,7 @@ __device__ __forceinline__ bool bf_ok(const SweepArgs& a, unsigned long long p, 
 
 __global__ void __launch_bounds__(kTB) k_sweep_tile(SweepArgs a)
 {
-    __shared__ float4 s_box[kTile];
-    __shared__ uint4 s_vid[kTile];
+    __shared__ float4 s_box[kTile + 4];
     __shared__ unsigned s_span;
     const unsigned long long B = a.range[0], E = a.range[1];
     const unsigned long long base = a.row0 + static_cast<unsigned long long>(blockIdx.x) * kTB;
@@ -376,20 +375,43 @@ __global__ void __launch_bounds__(kTB) k_sweep_tile(SweepArgs a)
     const unsigned w_hi = __reduce_max_sync(0xffffffffu, (row && je_off > jb_off) ? je_off : 0u);
     __syncthreads();
     const unsigned span = s_span;
+    // per-lane window [jb_off, je_off) as (start, length): one unsigned
+    // compare tests both ends
+    const unsigned len = (row && je_off > jb_off) ? je_off - jb_off : 0u;
     for (unsigned c0 = 1; c0 < span; c0 += kTile) {
         const unsigned n = min(static_cast<unsigned>(kTile), span - c0);
-        for (unsigned t = threadIdx.x; t < n; t += kTB) {
+        for (unsigned t = threadIdx.x; t < n; t += kTB)
             s_box[t] = a.sbox[base + c0 + t];
-            s_vid[t] = a.svid[base + c0 + t];
-        }
         __syncthreads();
         const unsigned j0 = max(c0, w_lo), j1 = min(c0 + n, w_hi);
-        for (unsigned j = j0; j < j1; ++j) {
-            const float4 o = s_box[j - c0];
-            const bool hit = j >= jb_off && j < je_off && box_hit(mb, o);
-            if (__any_sync(0xffffffffu, hit)) {
-                const uint4 ov = s_vid[j - c0];
-                const bool keep = hit && keep_pair(mv, ov) && bf_ok(a, p, base + j);
+        const float4* sp = s_box - c0;
+        unsigned j = j0;
+        // 4 boxes per vote: LDS.128 broadcast + 4 compares + 1 range test each
+        for (; j + 4 <= j1; j += 4) {
+            const float4 o0 = sp[j], o1 = sp[j + 1], o2 = sp[j + 2], o3 = sp[j + 3];
+            const bool h0 = (j - jb_off) < len && box_hit(mb, o0);
+            const bool h1 = (j + 1 - jb_off) < len && box_hit(mb, o1);
+            const bool h2 = (j + 2 - jb_off) < len && box_hit(mb, o2);
+            const bool h3 = (j + 3 - jb_off) < len && box_hit(mb, o3);
+            if (__any_sync(0xffffffffu, h0 | h1 | h2 | h3)) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool h = u == 0 ? h0 : u == 1 ? h1 : u == 2 ? h2 : h3;
+                    if (__any_sync(0xffffffffu, h)) {
+                        const unsigned long long q = base + j + u;
+                        const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
+                        const bool keep = h && keep_pair(mv, ov) && bf_ok(a, p, q);
+                        emit(a, keep, mv.w, ov.w);
+                    }
+                }
+            }
+        }
+        for (; j < j1; ++j) {
+            const bool h = (j - jb_off) < len && box_hit(mb, sp[j]);
+            if (__any_sync(0xffffffffu, h)) {
+                const unsigned long long q = base + j;
+                const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
+                const bool keep = h && keep_pair(mv, ov) && bf_ok(a, p, q);
                 emit(a, keep, mv.w, ov.w);
             }
         }

@@ -254,7 +254,7 @@ struct Ctx {
     bool last_pairs_general = false;
 
     // queries / narrow phase
-    DevBuf q_kind, q_points, q_sep;
+    DevBuf q_kind, q_points, q_sep, q_flags;
     DevBuf iv_qid[2], iv_t[2], iv_u[2], iv_v[2], iv_dep[2];
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
     DevBuf nscal;                      // NarrowScalars

@@ -116,9 +116,19 @@ struct Eval {
 // The hull starts from corner 0 like the reference; min/max of the remaining
 // corners is order-independent (bounds are never +/-0 after widening, and a
 // NaN operand is ignored by std::min/max unless it is the running value).
-template <class W>
-__device__ __forceinline__ void evaluate(bool vf, const double* __restrict__ P, const Box& b,
-                                         Eval& ev)
+// Coordinate sources: a global query record (24 doubles) or a lane's column
+// of a transposed shared-memory stage (element e at base[32 * e]).
+struct GlobalPts {
+    const double* __restrict__ p;
+    __device__ __forceinline__ double operator()(int e) const { return __ldg(p + e); }
+};
+struct SmemPts {
+    const double* p;
+    __device__ __forceinline__ double operator()(int e) const { return p[32 * e]; }
+};
+
+template <class W, class Pts>
+__device__ __forceinline__ void evaluate(bool vf, const Pts& P, const Box& b, Eval& ev)
 {
     ev.infl[0] = ev.infl[1] = ev.infl[2] = 0.0;
 #pragma unroll
@@ -127,8 +137,8 @@ __device__ __forceinline__ void evaluate(bool vf, const double* __restrict__ P, 
         I dl[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            x0[p] = __ldg(P + 3 * p + c);
-            const double x1 = __ldg(P + 12 + 3 * p + c);
+            x0[p] = P(3 * p + c);
+            const double x1 = P(12 + 3 * p + c);
             const double d = __dsub_rn(x1, x0[p]); // point(x1) - point(x0): both bounds
             dl[p] = { W::dn(d), W::up(d) };
         }
@@ -206,8 +216,8 @@ enum : int { kPruned = 0, kCollision = 1, kSplit = 2 };
 
 // process_interval (narrowphase.cpp:134-187).  Returns the action; for Split
 // `dim` is the bisection dimension (0 t, 1 u, 2 v).
-template <class W>
-__device__ __forceinline__ int process_one(bool vf, const double* __restrict__ P, const Box& b,
+template <class W, class Pts>
+__device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
                                            double t_star, double d, const Cfg& cfg,
                                            double& cand_t, bool& zdiag, int& dim,
                                            bool& evaluated)
@@ -220,7 +230,7 @@ __device__ __forceinline__ int process_one(bool vf, const double* __restrict__ P
     if (vf && __dadd_rn(b.ulo, b.vlo) > 1.0)
         return kPruned;
     Eval ev;
-    evaluate<W>(vf, P, b, ev);
+    evaluate<W, Pts>(vf, P, b, ev);
     evaluated = true;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
@@ -263,14 +273,19 @@ __device__ __forceinline__ int process_one(bool vf, const double* __restrict__ P
 
 // A query takes the Fast widening when every coordinate is <= 2^1000 in
 // magnitude (see the header comment).
-__device__ __forceinline__ bool fast_ok(const double* __restrict__ P)
+template <class Pts>
+__device__ __forceinline__ bool fast_ok(const Pts& P)
 {
     bool ok = true;
 #pragma unroll
     for (int i = 0; i < 24; ++i)
-        ok = ok && fabs(__ldg(P + i)) <= kFastLimit; // NaN compares false -> Exact
+        ok = ok && fabs(P(i)) <= kFastLimit; // NaN compares false -> Exact
     return ok;
 }
+
+// Query kind byte as stored on the device: bit0 = edge-edge, bit1 = the query
+// needs the Exact widening (set once per narrow phase by the init kernel).
+constexpr uint8_t kKindEE = 1, kKindExact = 2;
 
 } // namespace iv
 } // namespace ccdk

@@ -29,6 +29,7 @@ constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr int kGenBlock = 128;
 
 struct GenArgs {
+    uint8_t* qf;       // per-query kind | exact-widening flag (iv::kKind*)
     const uint8_t* kind;
     const double* pts;
     const double* sep;
@@ -64,9 +65,49 @@ __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned v)
         atomicAdd(dst, static_cast<unsigned long long>(s));
 }
 
-// One BFS generation: process_interval on every live interval + the fold.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Per-warp smem stage: 24 coordinates x 32 lanes, transposed (element-major)
+// so a warp reading element e touches 32 consecutive doubles.
+constexpr int kStageDoubles = 24 * 32;
+constexpr int kGenSmem = (kGenBlock / 32) * 2 * kStageDoubles * sizeof(double);
+
+struct Prefetch {
+    unsigned q;
+    double tlo, ulo, vlo;
+    unsigned long long dp;
+    unsigned exh;
+    unsigned long long snap;
+    double sep;
+    uint8_t qf;
+    bool valid;
+};
+
+__device__ __forceinline__ void stage_coords(const GenArgs& a, double* stage, unsigned lane, unsigned q)
+{
+    const double* src = a.pts + 24ull * q;
+#pragma unroll
+    for (int e = 0; e < 24; ++e)
+        cp_async8(stage + 32 * e + lane, src + e);
+}
+
+// One BFS generation: process_interval on every live interval + the fold
+// (narrowphase.cpp:226-305).  Each warp walks batches of 32 intervals with a
+// two-deep software pipeline: while batch b is evaluated from shared memory,
+// batch b+1's query coordinates stream in with cp.async and its interval
+// record and per-query scalars are already in flight into registers, and
+// batch b+2's query ids are being loaded.  The evaluation (~1.4k fp64/ALU
+// instructions per interval) hides all three latencies.
 __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
 {
+    extern __shared__ double gsm[];
     NarrowScalars* sc = a.sc;
     if (!sc->cont)
         return;
@@ -79,26 +120,63 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
     const double* __restrict__ vs = a.v[cb];
     const unsigned long long* __restrict__ ds = a.dep[cb];
     const unsigned lane = threadIdx.x & 31;
-    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    const unsigned wib = threadIdx.x >> 5;
+    double* stages = gsm + wib * 2 * kStageDoubles;
+    const unsigned long long nbatch = (n + 31) >> 5;
+    const unsigned long long W = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long b = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x >> 5) + wib;
     unsigned evals = 0, split_actions = 0, dropped = 0;
+    if (b >= nbatch)
+        return; // warp-uniform; no __syncthreads in this kernel
 
-    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x
-             + (threadIdx.x & ~31u);
-         base < n; base += stride) {
-        const unsigned long long i = base + lane;
+    auto fetch = [&](unsigned long long bb, unsigned q, Prefetch& f) {
+        const unsigned long long i = (bb << 5) + lane;
+        f.valid = bb < nbatch && i < n;
+        if (f.valid) {
+            f.q = q;
+            f.tlo = ts[i];
+            f.ulo = us[i];
+            f.vlo = vs[i];
+            f.dp = ds[i];
+            f.exh = a.exh_gen[q];
+            f.snap = a.snap[q];
+            f.sep = a.sep ? a.sep[q] : a.sep_default;
+            f.qf = a.qf[q];
+        }
+    };
+    auto load_q = [&](unsigned long long bb) -> unsigned {
+        const unsigned long long i = (bb << 5) + lane;
+        return (bb < nbatch && i < n) ? qid[i] : 0u;
+    };
+
+    // prologue: batch b's coordinates + record, batch b+W's query id
+    Prefetch cur;
+    {
+        const unsigned q0 = load_q(b);
+        fetch(b, q0, cur);
+        if (cur.valid)
+            stage_coords(a, stages, lane, q0);
+        cp_async_commit();
+    }
+    unsigned q_next = load_q(b + W);
+    int st = 0;
+
+    for (; b < nbatch; b += W) {
+        // issue batch b+W: coordinates into the other stage, record + scalars
+        Prefetch nxt;
+        fetch(b + W, q_next, nxt);
+        if (nxt.valid)
+            stage_coords(a, stages + (st ^ 1) * kStageDoubles, lane, q_next);
+        cp_async_commit();
+        q_next = load_q(b + 2 * W);
+        cp_async_wait<1>(); // batch b's copies (this lane's own) have landed
+
         bool admit = false;
-        unsigned q = 0;
-        double tlo = 0, ulo = 0, vlo = 0;
-        unsigned long long dp = 0;
         int dim = -1;
-        if (i < n) {
-            q = qid[i];
-            tlo = ts[i];
-            ulo = us[i];
-            vlo = vs[i];
-            dp = ds[i];
-            const unsigned dt = dp & 0xffff, du = (dp >> 16) & 0xffff, dv = (dp >> 32) & 0xffff;
-            if (a.exh_gen[q] < gen) {
+        if (cur.valid) {
+            const unsigned q = cur.q;
+            const double tlo = cur.tlo;
+            if (cur.exh < gen) {
                 // exhausted in an earlier generation: fold t.lo and drop
                 // (narrowphase.cpp:280-291)
                 atomicMin(&a.toi[q], dbits(tlo));
@@ -106,29 +184,29 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
                     a.zdiag[q] = 1;
                 ++dropped;
             } else {
-                iv::Box b;
-                b.tlo = tlo;
-                b.thi = __dadd_rn(tlo, iv::dyadic_width(dt));
-                b.ulo = ulo;
-                b.uhi = __dadd_rn(ulo, iv::dyadic_width(du));
-                b.vlo = vlo;
-                b.vhi = __dadd_rn(vlo, iv::dyadic_width(dv));
-                const double t_star = __longlong_as_double(static_cast<long long>(a.snap[q]));
-                const double d = a.sep ? a.sep[q] : a.sep_default;
-                const bool vf = a.kind[q] == CCDK_QUERY_VF;
-                const double* P = a.pts + 24ull * q;
+                const unsigned long long dp = cur.dp;
+                iv::Box bx;
+                bx.tlo = tlo;
+                bx.thi = __dadd_rn(tlo, iv::dyadic_width(dp & 0xffff));
+                bx.ulo = cur.ulo;
+                bx.uhi = __dadd_rn(cur.ulo, iv::dyadic_width((dp >> 16) & 0xffff));
+                bx.vlo = cur.vlo;
+                bx.vhi = __dadd_rn(cur.vlo, iv::dyadic_width((dp >> 32) & 0xffff));
+                const double t_star = __longlong_as_double(static_cast<long long>(cur.snap));
+                const bool vf = !(cur.qf & iv::kKindEE);
+                const iv::SmemPts P { stages + st * kStageDoubles + lane };
                 double cand = 0;
                 bool zd = false, evald = false;
                 int act;
-                if (iv::fast_ok(P))
-                    act = iv::process_one<iv::Fast>(vf, P, b, t_star, d, a.cfg, cand, zd, dim, evald);
+                if (!(cur.qf & iv::kKindExact))
+                    act = iv::process_one<iv::Fast>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
                 else
-                    act = iv::process_one<iv::Exact>(vf, P, b, t_star, d, a.cfg, cand, zd, dim, evald);
+                    act = iv::process_one<iv::Exact>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
                 evals += evald;
                 if (act == iv::kCollision) {
-                    const unsigned long long cb2 = dbits(cand);
-                    const unsigned long long old = atomicMin(&a.toi[q], cb2);
-                    if (cb2 < old && atomicExch(&a.dirty_mark[q], gen + 1) != gen + 1)
+                    const unsigned long long cbits = dbits(cand);
+                    const unsigned long long old = atomicMin(&a.toi[q], cbits);
+                    if (cbits < old && atomicExch(&a.dirty_mark[q], gen + 1) != gen + 1)
                         a.dirty[atomicAdd(&sc->dirty_n, 1ull)] = q;
                     if (zd)
                         a.zdiag[q] = 1;
@@ -158,19 +236,20 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
             if (admit) {
                 const unsigned long long s = slot0 + 2ull * __popc(mask & ((1u << lane) - 1));
                 if (s + 2 <= a.phys_cap) {
+                    const unsigned long long dp = cur.dp;
                     const unsigned dd = (dp >> (16 * dim)) & 0xffff;
-                    const double lo = dim == 0 ? tlo : dim == 1 ? ulo : vlo;
+                    const double lo = dim == 0 ? cur.tlo : dim == 1 ? cur.ulo : cur.vlo;
                     // split_box (narrowphase.cpp:122-132): exact midpoint
                     const double mid = __dadd_rn(lo, __dmul_rn(0.5, iv::dyadic_width(dd)));
                     const unsigned long long dpc = dp + (1ull << (16 * dim));
-                    a.qid[nb][s] = q;
-                    a.qid[nb][s + 1] = q;
-                    a.t[nb][s] = tlo;
-                    a.t[nb][s + 1] = dim == 0 ? mid : tlo;
-                    a.u[nb][s] = ulo;
-                    a.u[nb][s + 1] = dim == 1 ? mid : ulo;
-                    a.v[nb][s] = vlo;
-                    a.v[nb][s + 1] = dim == 2 ? mid : vlo;
+                    a.qid[nb][s] = cur.q;
+                    a.qid[nb][s + 1] = cur.q;
+                    a.t[nb][s] = cur.tlo;
+                    a.t[nb][s + 1] = dim == 0 ? mid : cur.tlo;
+                    a.u[nb][s] = cur.ulo;
+                    a.u[nb][s + 1] = dim == 1 ? mid : cur.ulo;
+                    a.v[nb][s] = cur.vlo;
+                    a.v[nb][s + 1] = dim == 2 ? mid : cur.vlo;
                     a.dep[nb][s] = dpc;
                     a.dep[nb][s + 1] = dpc;
                 } else {
@@ -178,7 +257,10 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
                 }
             }
         }
+        cur = nxt;
+        st ^= 1;
     }
+    cp_async_wait<0>();
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);
     warp_add(&sc->dropped, dropped);
@@ -225,7 +307,8 @@ __global__ void k_finish(GenArgs a)
     __threadfence();
 }
 
-__global__ void k_init_queries(unsigned long long n, unsigned long long* toi,
+__global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const double* pts,
+                               uint8_t* qf, unsigned long long* toi,
                                unsigned long long* snap, unsigned long long* splits,
                                unsigned* exh_gen, uint8_t* zdiag, unsigned* dirty_mark,
                                uint32_t* qid, double* t, double* u, double* v,
@@ -240,6 +323,8 @@ __global__ void k_init_queries(unsigned long long n, unsigned long long* toi,
         zdiag[q] = 0;
         dirty_mark[q] = 0;
         qid[q] = static_cast<uint32_t>(q); // one root box [0,1]^3 per query
+        qf[q] = static_cast<uint8_t>((kind[q] == CCDK_QUERY_EE ? iv::kKindEE : 0)
+                                     | (iv::fast_ok(iv::GlobalPts { pts + 24 * q }) ? 0 : iv::kKindExact));
         t[q] = 0.0;
         u[q] = 0.0;
         v[q] = 0.0;
@@ -292,7 +377,7 @@ __global__ void k_inclusion(const uint8_t* kind, const double* pts, const double
     const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (i >= n)
         return;
-    const double* P = pts + 24 * i;
+    const iv::GlobalPts P { pts + 24 * i };
     const double* bx = boxes + 6 * i;
     const iv::Box b { bx[0], bx[1], bx[2], bx[3], bx[4], bx[5] };
     iv::Eval ev;
@@ -316,7 +401,7 @@ __global__ void k_process(const uint8_t* kind, const double* pts, const double* 
     const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (i >= n)
         return;
-    const double* P = pts + 24 * i;
+    const iv::GlobalPts P { pts + 24 * i };
     const double* bx = boxes + 6 * i;
     const iv::Box b { bx[0], bx[1], bx[2], bx[3], bx[4], bx[5] };
     const double d = (sep && sep[i] >= 0.0) ? sep[i] : sep_default;
@@ -440,6 +525,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         return false;
     GenArgs a {};
     a.kind = kind;
+    a.qf = grow<uint8_t>(c.q_flags, n);
     a.pts = pts;
     a.sep = sep;
     a.sep_default = in.cfg.min_separation;
@@ -470,13 +556,19 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, &init, sizeof init, cudaMemcpyHostToDevice, s));
     const dim3 ig = grid_for(n, 256);
     k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(
-        n, a.toi, a.snap, a.splits, a.exh_gen, a.zdiag, a.dirty_mark, a.qid[0], a.t[0], a.u[0],
+        n, kind, pts, a.qf, a.toi, a.snap, a.splits, a.exh_gen, a.zdiag, a.dirty_mark, a.qid[0], a.t[0], a.u[0],
         a.v[0], a.dep[0]);
     CCDK_LAUNCH_CHECK();
 
     int blocks_per_sm = 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CCDK_CUDA_CHECK(cudaFuncSetAttribute(k_generation, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenSmem));
+        CCDK_CUDA_CHECK(cudaFuncSetAttribute(k_generation, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr_set = true;
+    }
     CCDK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_generation,
-                                                                  kGenBlock, 0));
+                                                                  kGenBlock, kGenSmem));
     const unsigned gen_grid = static_cast<unsigned>(std::max(1, blocks_per_sm) * c.num_sms);
     const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
 
@@ -485,7 +577,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     static const bool debug = getenv("CCDK_DEBUG") != nullptr;
     for (;;) {
         for (int g = 0; g < batch; ++g) {
-            k_generation<<<gen_grid, kGenBlock, 0, s>>>(a);
+            k_generation<<<gen_grid, kGenBlock, kGenSmem, s>>>(a);
             k_finish<<<fin_grid, 256, 0, s>>>(a);
         }
         c.narrow_launches += 2 * batch;
