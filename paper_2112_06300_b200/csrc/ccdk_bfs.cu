@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
 
         bool admit = false;
         int dim = -1;
+        unsigned long long split_old = 0;
         if (cur.valid) {
             const unsigned q = cur.q;
             const double tlo = cur.tlo;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
                 if (!(cur.qf & iv::kKindExact))
                     act = iv::process_one<iv::Fast>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
                 else
-                    act = iv::process_one<iv::Exact>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
+                    act = iv::process_exact<iv::SmemPts>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
                 evals += evald;
                 if (act == iv::kCollision) {
                     const unsigned long long cbits = dbits(cand);
@@ -211,17 +212,20 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
                     if (zd)
                         a.zdiag[q] = 1;
                 } else if (act == iv::kSplit) {
+                    // Every split is appended; the request counter's old value
+                    // is consumed only after the append (its round trip
+                    // overlaps the cursor atomic).  A request beyond the
+                    // budget marks the query exhausted in this generation;
+                    // its children are then folded (min t.lo, zdiag at
+                    // t.lo == 0) and dropped at the start of the next one,
+                    // which equals the reference's fold of every split
+                    // interval of the exhausting generation
+                    // (narrowphase.cpp:254-297): a child's t.lo is >= its
+                    // parent's and the left child's equals it.
                     ++split_actions;
-                    const bool exempt = a.cfg.no_zero_toi && tlo == 0.0;
-                    if (exempt || atomicAdd(&a.splits[q], 1ull) < a.max_splits) {
-                        admit = true;
-                    } else {
-                        // budget exhausted (narrowphase.cpp:263-271)
-                        atomicMin(&a.toi[q], dbits(tlo));
-                        a.exh_gen[q] = gen;
-                        if (a.cfg.no_zero_toi && tlo == 0.0)
-                            a.zdiag[q] = 1;
-                    }
+                    admit = true;
+                    if (!(a.cfg.no_zero_toi && tlo == 0.0))
+                        split_old = atomicAdd(&a.splits[q], 1ull);
                 }
             }
         }
@@ -257,6 +261,8 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
                 }
             }
         }
+        if (split_old >= a.max_splits)
+            a.exh_gen[cur.q] = gen; // budget exhausted (narrowphase.cpp:263-271)
         cur = nxt;
         st ^= 1;
     }

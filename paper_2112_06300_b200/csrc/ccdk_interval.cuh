@@ -127,12 +127,13 @@ struct SmemPts {
     __device__ __forceinline__ double operator()(int e) const { return p[32 * e]; }
 };
 
+// One component c of evaluate_box: the hull `rng` of the 8 corners and the
+// component's contribution to the three influences.
 template <class W, class Pts>
-__device__ __forceinline__ void evaluate(bool vf, const Pts& P, const Box& b, Eval& ev)
+__device__ __forceinline__ void component(bool vf, const Pts& P, const Box& b, int c, I& rng,
+                                          double infl[3])
 {
-    ev.infl[0] = ev.infl[1] = ev.infl[2] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
+    {
         double x0[4];
         I dl[4];
 #pragma unroll
@@ -143,7 +144,6 @@ __device__ __forceinline__ void evaluate(bool vf, const Pts& P, const Box& b, Ev
             dl[p] = { W::dn(d), W::up(d) };
         }
         double m0[4]; // corner midpoints at t = lo, indexed by (u bit) | (v bit) << 1
-        I rng;
 #pragma unroll
         for (int tb = 0; tb < 2; ++tb) {
             const double t = tb ? b.thi : b.tlo;
@@ -182,10 +182,10 @@ __device__ __forceinline__ void evaluate(bool vf, const Pts& P, const Box& b, Ev
                 m[uv] = mid2(f);
             }
             // u influence: corners differing in bit1; v influence: bit2
-            ev.infl[1] = smax(ev.infl[1], fabs(__dsub_rn(m[1], m[0])));
-            ev.infl[1] = smax(ev.infl[1], fabs(__dsub_rn(m[3], m[2])));
-            ev.infl[2] = smax(ev.infl[2], fabs(__dsub_rn(m[2], m[0])));
-            ev.infl[2] = smax(ev.infl[2], fabs(__dsub_rn(m[3], m[1])));
+            infl[1] = smax(infl[1], fabs(__dsub_rn(m[1], m[0])));
+            infl[1] = smax(infl[1], fabs(__dsub_rn(m[3], m[2])));
+            infl[2] = smax(infl[2], fabs(__dsub_rn(m[2], m[0])));
+            infl[2] = smax(infl[2], fabs(__dsub_rn(m[3], m[1])));
             if (tb == 0) {
 #pragma unroll
                 for (int uv = 0; uv < 4; ++uv)
@@ -193,11 +193,19 @@ __device__ __forceinline__ void evaluate(bool vf, const Pts& P, const Box& b, Ev
             } else {
 #pragma unroll
                 for (int uv = 0; uv < 4; ++uv)
-                    ev.infl[0] = smax(ev.infl[0], fabs(__dsub_rn(m[uv], m0[uv])));
+                    infl[0] = smax(infl[0], fabs(__dsub_rn(m[uv], m0[uv])));
             }
         }
-        ev.range[c] = rng;
     }
+}
+
+template <class W, class Pts>
+__device__ __forceinline__ void evaluate(bool vf, const Pts& P, const Box& b, Eval& ev)
+{
+    ev.infl[0] = ev.infl[1] = ev.infl[2] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        component<W, Pts>(vf, P, b, c, ev.range[c], ev.infl);
 }
 
 // splittable (narrowphase.cpp:109-113)
@@ -229,22 +237,28 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
         return kPruned;
     if (vf && __dadd_rn(b.ulo, b.vlo) > 1.0)
         return kPruned;
+    // Components one at a time (rolled loop: a third of the code, so the hot
+    // loop stays in the instruction cache).  A component whose range misses
+    // the tolerance cube prunes the box whatever the others hold, so the loop
+    // exits early; otherwise the inside test, max width and influences are
+    // reduced on the fly (all order-independent).
     Eval ev;
-    evaluate<W, Pts>(vf, P, b, ev);
+    ev.infl[0] = ev.infl[1] = ev.infl[2] = 0.0;
     evaluated = true;
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        if (ev.range[c].lo > d || ev.range[c].hi < -d)
+    bool inside = true;
+    double wmax = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        I rng;
+        component<W, Pts>(vf, P, b, c, rng, ev.infl);
+        if (rng.lo > d || rng.hi < -d)
             return kPruned;
+        inside = inside && rng.lo >= -d && rng.hi <= d;
+        const double w = __dsub_rn(rng.hi, rng.lo);
+        wmax = c == 0 ? w : smax(wmax, w);
+    }
     const bool force_zero = cfg.no_zero_toi && b.tlo == 0.0;
     if (!force_zero) {
-        bool inside = true;
-        double wmax = __dsub_rn(ev.range[0].hi, ev.range[0].lo);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            inside = inside && ev.range[c].lo >= -d && ev.range[c].hi <= d;
-            wmax = smax(wmax, __dsub_rn(ev.range[c].hi, ev.range[c].lo));
-        }
         if (wmax < cfg.delta || inside) {
             cand_t = b.tlo;
             return kCollision;
@@ -273,6 +287,16 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 
 // A query takes the Fast widening when every coordinate is <= 2^1000 in
 // magnitude (see the header comment).
+// The Exact-widening instantiation is out of line: it runs only for queries
+// beyond 2^1000 and would otherwise double the hot loop's code size.
+template <class Pts>
+__device__ __noinline__ int process_exact(bool vf, const Pts P, const Box b, double t_star,
+                                          double d, const Cfg cfg, double& cand_t, bool& zdiag,
+                                          int& dim, bool& evaluated)
+{
+    return process_one<Exact, Pts>(vf, P, b, t_star, d, cfg, cand_t, zdiag, dim, evaluated);
+}
+
 template <class Pts>
 __device__ __forceinline__ bool fast_ok(const Pts& P)
 {
