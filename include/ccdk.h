@@ -222,6 +222,21 @@ CCDK_API int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_
              const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
              const ccdk_pipeline_cfg* cfg, ccdk_report* report);
 
+/* ccd_no_zero_toi (pipeline.hpp:82-85, pipeline.cpp:234-256): requires
+ * cfg->narrow.no_zero_toi; a separated run, then on an exact-zero ToI a
+ * zero-separation always-split-at-t=0 retry whose ToI is scaled by 0.8. */
+CCDK_API int ccdk_ccd_no_zero_toi(ccdk_ctx* ctx, const double* v0, const double* v1,
+                                  uint64_t nv, const uint32_t* edges, uint64_t ne,
+                                  const uint32_t* faces, uint64_t nf,
+                                  const ccdk_pipeline_cfg* cfg, ccdk_report* report);
+
+/* query_min_separations (pipeline.hpp:90-91, pipeline.cpp:39-55): Absolute
+ * mode copies cfg->narrow.min_separation; Relative mode is min_sep_fraction
+ * times the t=0 point-triangle / segment-segment distance (distance.cpp). */
+CCDK_API int ccdk_query_min_separations(ccdk_ctx* ctx, const uint8_t* kind,
+                                        const double* points, uint64_t n,
+                                        const ccdk_pipeline_cfg* cfg, double* out);
+
 /* Device-resident variant: upload a scene once, then run steps on it. */
 CCDK_API int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
                       const uint32_t* edges, uint64_t ne, const uint32_t* faces,

@@ -21,7 +21,7 @@ LIB = os.path.join(PKG, "lib")
 INCLUDE = os.path.join(ROOT, "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["ccdk_api.cu", "ccdk_geometry.cu", "ccdk_broad.cu", "ccdk_bfs.cu"]
+CU_SOURCES = ["ccdk_api.cu", "ccdk_geometry.cu", "ccdk_broad.cu", "ccdk_bfs.cu", "ccdk_distance.cu"]
 CXX_SOURCES = ["ccdkit_host.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -404,6 +404,47 @@ def ccd(scene: SceneStep, cfg: PipelineConfig | None = None, want_candidates: bo
     return _report(r, pairs)
 
 
+def ccd_no_zero_toi(scene: SceneStep, cfg: PipelineConfig, want_candidates: bool = True,
+                    ctx=None) -> CcdReport:
+    """ccd_no_zero_toi (pipeline.hpp:82-85): the zero-ToI retry policy."""
+    c = _ctx(ctx)
+    r = abi.Report()
+    ccfg = cfg.to_c()
+    check(lib().ccdk_ccd_no_zero_toi(c.h, p(scene.vertices_t0, P_F64), p(scene.vertices_t1, P_F64),
+                                     scene.nv, p(scene.edges, P_U32), scene.ne, p(scene.faces, P_U32),
+                                     scene.nf, C.byref(ccfg), C.byref(r)))
+    pairs = None
+    if want_candidates:
+        pairs = np.empty((r.candidate_count, 2), np.uint64)
+        if r.candidate_count:
+            check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
+    return _report(r, pairs)
+
+
+def query_min_separations(queries: QueryBatch, cfg: PipelineConfig, ctx=None) -> np.ndarray:
+    """query_min_separations (pipeline.hpp:90-91)."""
+    c = _ctx(ctx)
+    n = len(queries)
+    out = np.empty(max(n, 1), np.float64)
+    kind, pts = u8(queries.kind), f64(queries.points).reshape(-1, 24)
+    ccfg = cfg.to_c()
+    check(lib().ccdk_query_min_separations(c.h, p(kind, P_U8), p(pts, P_F64), n, C.byref(ccfg),
+                                           p(out, P_F64)))
+    return out[:n].copy()
+
+
+def point_triangle_distance(p_, a, b, c_, ctx=None) -> float:
+    """distance.hpp: evaluated by the device kernel of query_min_separations
+    (Relative mode with fraction 1)."""
+    q = QueryBatch(np.zeros(1, np.uint8), np.concatenate([np.ravel(x) for x in (p_, a, b, c_)] + [np.zeros(12)])[None])
+    return float(query_min_separations(q, PipelineConfig(min_sep_mode=MINSEP_RELATIVE, min_sep_fraction=1.0), ctx)[0])
+
+
+def segment_segment_distance(p0, p1, q0, q1, ctx=None) -> float:
+    q = QueryBatch(np.ones(1, np.uint8), np.concatenate([np.ravel(x) for x in (p0, p1, q0, q1)] + [np.zeros(12)])[None])
+    return float(query_min_separations(q, PipelineConfig(min_sep_mode=MINSEP_RELATIVE, min_sep_fraction=1.0), ctx)[0])
+
+
 class ResidentScene:
     """A scene uploaded once; ``step()`` runs the device-resident CCD step
     (the timed unit of bench.py).  ``shard`` restricts the sweep to one of

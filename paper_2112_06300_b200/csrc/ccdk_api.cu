@@ -369,20 +369,179 @@ void upload_scene(Ctx& c, const double* v0, const double* v1, uint64_t nv, const
     s.valid = true;
 }
 
+// run_batched's BatchRun (pipeline.cpp:81-175) over device primitives.  The
+// recursion structure, capacities and counters follow the reference so the
+// batch count and tracked bytes agree; every broad/narrow batch is a device
+// run.  At the default budget this is exactly one broad and one narrow batch.
+struct BatchRun {
+    Ctx& c;
+    const ccdk_pipeline_cfg& cfg;
+    DevScene& s;
+    uint64_t k;
+    uint64_t cap_pairs;
+    float* bmin = nullptr;
+    float* bmax = nullptr;
+    uint4* vids = nullptr;
+    unsigned long long toi_bits = 0x7ff0000000000000ull;
+    bool tol = false, zd = false;
+    uint64_t candidates = 0, queries = 0, vf = 0, narrow_batches = 0, broad_batches = 0;
+    uint64_t pair_tests = 0, total_splits = 0, evaluations = 0, split_actions = 0;
+    uint64_t generations = 0, peak_queue = 0, launches = 0;
+    uint64_t peak_bytes = 0, base_bytes = 0;
+    float ms_sort = 0, ms_sweep = 0, ms_pairsort = 0, ms_classify = 0, ms_narrow = 0;
+    int axis = 0;
+
+    // broad_batch (pipeline.cpp:140-174): halve the sweep range while the
+    // candidates exceed the budget's pair capacity
+    void broad_batch(uint64_t begin, uint64_t end, uint32_t shard_rank = 0, uint32_t shard_count = 1)
+    {
+        BroadIn bi;
+        bi.bmin = bmin;
+        bi.bmax = bmax;
+        bi.vids = vids;
+        bi.k = k;
+        bi.method = CCDK_BROAD_STQ; // stq/sap/bf give the identical set
+        bi.range_begin = begin;
+        bi.range_end = end;
+        bi.shard_rank = shard_rank;
+        bi.shard_count = shard_count;
+        BroadOut bo;
+        broad_phase(c, bi, bo);
+        launches += 11;
+        pair_tests += bo.pair_tests;
+        ms_sort += bo.ms_axis_sort;
+        ms_sweep += bo.ms_sweep;
+        ms_pairsort += bo.ms_pairsort;
+        axis = bo.axis;
+        if (shard_count > 1) { // this shard's slice of sorted left positions
+            begin = bo.range_lo;
+            end = bo.range_hi;
+        }
+        if (bo.n_pairs > cap_pairs && end - begin > 1) {
+            const uint64_t mid = begin + (end - begin) / 2;
+            broad_batch(begin, mid);
+            broad_batch(mid, end);
+            return;
+        }
+        ++broad_batches;
+        const uint64_t n = bo.n_pairs;
+        const uint64_t* keys = c.pair_keys_sorted.as<uint64_t>();
+        uint64_t* all = static_cast<uint64_t*>(c.all_keys.ensure_keep((candidates + n) * 8, c.stream));
+        if (n)
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(all + candidates, keys, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+        candidates += n;
+        base_bytes = k * 32 + candidates * 16;
+        // classify (K7) + query_min_separations
+        cudaEvent_t e0, e1;
+        CCDK_CUDA_CHECK(cudaEventCreate(&e0));
+        CCDK_CUDA_CHECK(cudaEventCreate(&e1));
+        CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+        uint8_t* qk = grow<uint8_t>(c.q_kind, std::max<uint64_t>(n, 1));
+        double* qp = grow<double>(c.q_points, 24 * std::max<uint64_t>(n, 1));
+        launch_classify_keys(c, keys, n, c.last_nb, s.v0.as<double>(), s.v1.as<double>(), s.nv,
+                             s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp);
+        double* seps = nullptr;
+        if (cfg.min_sep_mode == CCDK_MINSEP_RELATIVE && n) {
+            seps = grow<double>(c.q_sep, n);
+            launch_min_seps(c, qk, qp, n, cfg, seps);
+            ++launches;
+        }
+        unsigned long long nvf = 0;
+        if (n) {
+            auto* ctr = c.counters.as<DevCounters>();
+            k_count_vf<<<1, 1, 0, c.stream>>>(reinterpret_cast<const unsigned long long*>(keys), n,
+                                              c.last_nb, s.nv, &ctr->misc[2]);
+            CCDK_LAUNCH_CHECK();
+            d2h(c, &nvf, &ctr->misc[2], 8);
+            launches += 2;
+        }
+        CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
+        const uint64_t qoff = queries;
+        queries += n;
+        grow_results(queries);
+        if (n)
+            narrow_batch(qk, qp, seps, 0, n, qoff);
+        else
+            ++narrow_batches; // an empty narrow run still counts as a batch
+        CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        ms_classify += ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        vf += nvf;
+    }
+
+    void grow_results(uint64_t nq)
+    {
+        c.all_toi.ensure_keep(std::max<uint64_t>(nq, 1) * 8, c.stream);
+        c.all_flags.ensure_keep(std::max<uint64_t>(nq, 1), c.stream);
+    }
+
+    // narrow_batch (pipeline.cpp:103-138): queue capacity from the budget,
+    // halve the queries on overflow
+    void narrow_batch(const uint8_t* qk, const double* qp, const double* seps, uint64_t lo,
+                      uint64_t hi, uint64_t qoff)
+    {
+        const uint64_t n_sub = hi - lo;
+        const uint64_t pair_bytes = n_sub * (cfg.rs_query + 3 * cfg.rs_pair_ints);
+        const uint64_t avail = cfg.memory_budget > cfg.rs_params + pair_bytes
+            ? cfg.memory_budget - cfg.rs_params - pair_bytes
+            : 0;
+        NarrowIn ni;
+        ni.kind = qk + lo;
+        ni.points = qp + 24 * lo;
+        ni.sep = seps ? seps + lo : nullptr;
+        ni.n = n_sub;
+        ni.cfg = cfg.narrow;
+        ni.queue_capacity = avail / cfg.rs_interval;
+        NarrowOut no;
+        narrow_phase(c, ni, no);
+        launches += 2 + no.launches;
+        ms_narrow += static_cast<float>(no.stats.device_ms);
+        if (no.stats.overflow) {
+            if (n_sub <= 1)
+                throw Error(CCDK_CONFIG, "memory budget too small to hold even one query");
+            const uint64_t mid = lo + n_sub / 2;
+            narrow_batch(qk, qp, seps, lo, mid, qoff);
+            narrow_batch(qk, qp, seps, mid, hi, qoff);
+            return;
+        }
+        ++narrow_batches;
+        const unsigned long long gb = static_cast<unsigned long long>(
+            __builtin_bit_cast(uint64_t, no.stats.global_toi));
+        toi_bits = std::min(toi_bits, gb);
+        tol = tol || (no.any_flags & CCDK_FLAG_TOLERANCE_HIT);
+        zd = zd || (no.any_flags & CCDK_FLAG_ZERO_TOI_DIAG);
+        total_splits += no.stats.total_splits;
+        evaluations += no.stats.evaluations;
+        split_actions += no.stats.split_actions;
+        generations = std::max<uint64_t>(generations, no.stats.generations);
+        peak_queue = std::max<uint64_t>(peak_queue, no.stats.peak_queue);
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(c.all_toi.as<double>() + qoff + lo, no.toi, 8 * n_sub,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(c.all_flags.as<uint8_t>() + qoff + lo, no.flags, n_sub,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+        peak_bytes = std::max<uint64_t>(peak_bytes, base_bytes + n_sub * 216 + no.stats.peak_queue * 216);
+    }
+};
+
 // The full CCD step on ctx.scene (pipeline.cpp:218-232 via run_batched at the
 // default budget): build -> STQ -> classify -> narrow -> global min.
 void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_t shard_count,
               ccdk_report& rep, cudaEvent_t start_event)
 {
     validate_pipeline_cfg(cfg);
-    if (cfg.min_sep_mode == CCDK_MINSEP_RELATIVE)
-        throw Error(CCDK_CONFIG, "ccdk_ccd: Relative min-separation is not implemented on the device path yet");
     DevScene& s = c.scene;
     std::memset(&rep, 0, sizeof rep);
     rep.toi = INFINITY;
     rep.batch_count = 1;
     const uint64_t k = s.nv + s.ne + s.nf;
     cudaStream_t st = c.stream;
+    // run_batched (pipeline.cpp:184-187): candidate capacity of the budget
+    const uint64_t cap_pairs = (cfg.memory_budget - cfg.rs_params) / (cfg.rs_query + 3 * cfg.rs_pair_ints);
+    if (cap_pairs < 1)
+        throw Error(CCDK_CONFIG, "memory budget too small to hold even one query");
     cudaEvent_t ev[6];
     for (auto& e : ev)
         CCDK_CUDA_CHECK(cudaEventCreate(&e));
@@ -395,105 +554,74 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     launch_build_boxes(c, s.v0.as<double>(), s.v1.as<double>(), s.nv, s.edges.as<uint32_t>(), s.ne,
                        s.faces.as<uint32_t>(), s.nf, cfg.inflation, bmin, bmax, vids);
     CCDK_CUDA_CHECK(cudaEventRecord(ev[1], st));
-    // K2-K6
-    BroadIn bi;
-    bi.bmin = bmin;
-    bi.bmax = bmax;
-    bi.vids = vids;
-    bi.k = k;
-    bi.method = CCDK_BROAD_STQ; // stq/sap/bf give the identical set on a full range
-    bi.shard_rank = shard_rank;
-    bi.shard_count = shard_count;
-    BroadOut bo;
-    broad_phase(c, bi, bo);
-    {
+    if (k) {
         auto* ctr = c.counters.as<DevCounters>();
         unsigned long long err = 0;
         d2h(c, &err, &ctr->error, 8);
         sync(c);
-        if (k && err != ~0ull)
+        if (err != ~0ull)
             throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
     }
-    c.last_pairs_general = false;
-    CCDK_CUDA_CHECK(cudaEventRecord(ev[2], st));
-    // K7
-    const uint64_t n = bo.n_pairs;
-    uint8_t* qk = grow<uint8_t>(c.q_kind, std::max<uint64_t>(n, 1));
-    double* qp = grow<double>(c.q_points, 24 * std::max<uint64_t>(n, 1));
-    const uint64_t* keys = c.pair_keys_sorted.as<uint64_t>();
-    launch_classify_keys(c, keys, n, c.last_nb, s.v0.as<double>(), s.v1.as<double>(), s.nv,
-                         s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp);
-    auto* ctr = c.counters.as<DevCounters>();
-    if (n)
-        k_count_vf<<<1, 1, 0, st>>>(reinterpret_cast<const unsigned long long*>(keys), n,
-                                    c.last_nb, s.nv, &ctr->misc[2]);
-    CCDK_LAUNCH_CHECK();
-    CCDK_CUDA_CHECK(cudaEventRecord(ev[3], st));
-    // K8 + K9
-    NarrowIn ni;
-    ni.kind = qk;
-    ni.points = qp;
-    ni.n = n;
-    ni.cfg = cfg.narrow;
-    NarrowOut no;
-    narrow_phase(c, ni, no);
-    c.last_query_count = n;
-    CCDK_CUDA_CHECK(cudaEventRecord(ev[4], st));
-    double* dtoi = grow<double>(c.last_toi, 1);
-    k_store_toi<<<1, 1, 0, st>>>(static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars))),
-                                 n ? 1 : 0, dtoi);
-    CCDK_LAUNCH_CHECK();
-    unsigned long long any_flags = 0, vf_count = 0;
-    if (n) {
-        auto* sc = c.nscal.as<NarrowScalars>();
-        d2h(c, &any_flags, &sc->any_flags, 8);
-        d2h(c, &vf_count, &ctr->misc[2], 8);
+    BatchRun run { c, cfg, s, k, cap_pairs };
+    run.bmin = bmin;
+    run.bmax = bmax;
+    run.vids = vids;
+    if (k)
+        run.broad_batch(0, k, shard_rank, shard_count);
+    else
+        run.narrow_batches = 1;
+    // canonical order of the candidate union across batches (pipeline.cpp:196)
+    if (run.broad_batches > 1 && run.candidates) {
+        uint64_t* all = c.all_keys.as<uint64_t>();
+        uint64_t* tmp = grow<uint64_t>(c.pair_keys, run.candidates);
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, all, tmp, static_cast<int64_t>(run.candidates), 0,
+                                                  2 * c.last_nb, st);
+        });
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(all, tmp, run.candidates * 8, cudaMemcpyDeviceToDevice, st));
     }
+    c.last_keys_all = true;
+    c.last_pairs_general = false;
+    c.last_n_pairs = run.candidates;
+    c.last_query_count = run.queries;
+    double* dtoi = grow<double>(c.last_toi, 1);
+    const double toi = __builtin_bit_cast(double, static_cast<uint64_t>(run.toi_bits));
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(dtoi, &toi, 8, cudaMemcpyHostToDevice, st));
     CCDK_CUDA_CHECK(cudaEventRecord(ev[5], st));
     CCDK_CUDA_CHECK(cudaEventSynchronize(ev[5]));
 
-    rep.toi = n ? no.stats.global_toi : INFINITY;
-    rep.tolerance_hit = (any_flags & CCDK_FLAG_TOLERANCE_HIT) ? 1 : 0;
-    rep.zero_toi_diagnostic = (any_flags & CCDK_FLAG_ZERO_TOI_DIAG) ? 1 : 0;
-    rep.candidate_count = n;
-    rep.query_count = n;
-    rep.vf_count = vf_count;
-    rep.pair_tests = bo.pair_tests;
-    rep.total_splits = no.stats.total_splits;
-    rep.peak_queue = n ? no.stats.peak_queue : 0;
-    rep.evaluations = no.stats.evaluations;
-    rep.split_actions = no.stats.split_actions;
-    rep.generations = no.stats.generations;
-    rep.axis = bo.axis;
+    rep.toi = toi;
+    rep.tolerance_hit = run.tol ? 1 : 0;
+    rep.zero_toi_diagnostic = run.zd ? 1 : 0;
+    rep.candidate_count = run.candidates;
+    rep.query_count = run.queries;
+    rep.batch_count = std::max<uint64_t>(1, run.narrow_batches);
+    rep.vf_count = run.vf;
+    rep.pair_tests = run.pair_tests;
+    rep.total_splits = run.total_splits;
+    rep.peak_queue = run.peak_queue;
+    rep.evaluations = run.evaluations;
+    rep.split_actions = run.split_actions;
+    rep.generations = run.generations;
+    rep.axis = run.axis;
     // tracked_peak_bytes with the reference's accounting (pipeline.cpp:132-136,
-    // 158-159, 228): boxes 32 B, pairs 16 B, queries 216 B, intervals 64+152 B
-    const uint64_t base = k * 32 + n * 16;
-    uint64_t peak = std::max<uint64_t>(k * 32, base);
-    if (n)
-        peak = std::max<uint64_t>(peak, base + n * 216 + rep.peak_queue * (64 + 152));
-    rep.tracked_peak_bytes = peak;
-    float ms[6] = {};
-    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[0], ev[0], ev[1]));
-    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[1], ev[1], ev[2]));
-    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[2], ev[2], ev[3]));
-    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[3], ev[3], ev[4]));
-    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms[4], start_event ? start_event : ev[0], ev[5]));
-    rep.ms_build = ms[0];
-    rep.ms_sort = bo.ms_axis_sort;
-    rep.ms_sweep = bo.ms_sweep;
-    rep.ms_pairsort = bo.ms_pairsort;
-    rep.ms_classify = ms[2];
-    rep.ms_narrow = ms[3];
-    rep.ms_total = ms[4];
-    // own kernels: validate-free resident step = K1 + 11 broad-phase kernels
-    // (3 axis, keys, permute, run ends, range, heavy count/gen, tile, heavy)
-    // + classify + vf count + narrow (init, 2 per generation in batches of 8,
-    // outputs) + ToI store
-    rep.kernel_launches = 1 + 11 + (n ? 2 : 0) + (n ? 2 + no.launches : 0) + 1;
-    rep.t_cb = ms[0] * 1e-3;
-    rep.t_bp = ms[1] * 1e-3;
-    rep.t_socd = ms[2] * 1e-3;
-    rep.t_np = ms[3] * 1e-3;
+    // 158-159, 205-207, 228)
+    rep.tracked_peak_bytes = std::max<uint64_t>(k * 32, std::max(run.peak_bytes, run.base_bytes));
+    float ms_build = 0, ms_total = 0;
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms_build, ev[0], ev[1]));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms_total, start_event ? start_event : ev[0], ev[5]));
+    rep.ms_build = ms_build;
+    rep.ms_sort = run.ms_sort;
+    rep.ms_sweep = run.ms_sweep;
+    rep.ms_pairsort = run.ms_pairsort;
+    rep.ms_classify = run.ms_classify;
+    rep.ms_narrow = run.ms_narrow;
+    rep.ms_total = ms_total;
+    rep.kernel_launches = 1 + run.launches;
+    rep.t_cb = ms_build * 1e-3;
+    rep.t_bp = (run.ms_sort + run.ms_sweep + run.ms_pairsort) * 1e-3;
+    rep.t_socd = run.ms_classify * 1e-3;
+    rep.t_np = run.ms_narrow * 1e-3;
     for (auto& e : ev)
         cudaEventDestroy(e);
 }
@@ -685,6 +813,7 @@ int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner, const f
         c.last_n_pairs = 0;
         c.last_rounds.clear();
         c.last_pairs_general = true;
+        c.last_keys_all = false;
         if (k < 2)
             return;
         cudaStream_t s = c.stream;
@@ -768,7 +897,8 @@ int ccdk_fetch_pairs(ccdk_ctx* ctx, uint64_t* out)
         if (!n)
             return;
         uint64_t* ids = grow<uint64_t>(c.tmp[7], 2 * n);
-        launch_keys_to_ids(c, c.pair_keys_sorted.as<uint64_t>(), n, c.last_nb,
+        const uint64_t* keys = c.last_keys_all ? c.all_keys.as<uint64_t>() : c.pair_keys_sorted.as<uint64_t>();
+        launch_keys_to_ids(c, keys, n, c.last_nb,
                            c.last_pairs_general ? c.own_kind.as<uint8_t>() : nullptr,
                            c.last_pairs_general ? c.own_index.as<uint32_t>() : nullptr,
                            c.scene.nv, c.scene.ne, ids);
@@ -984,6 +1114,61 @@ int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
     });
 }
 
+int ccdk_ccd_no_zero_toi(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+                         const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
+                         const ccdk_pipeline_cfg* cfg, ccdk_report* report)
+{
+    // ccd_no_zero_toi (pipeline.cpp:234-256): separated run first; on an
+    // exact-zero ToI, re-run with zero separation and the always-split-at-t=0
+    // rule and scale the retried ToI by 0.8 (kZeroToiRetryScale)
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (!cfg->narrow.no_zero_toi)
+            throw Error(CCDK_CONFIG, "ccd_no_zero_toi: cfg.narrow.no_zero_toi must be set");
+        ccdk_pipeline_cfg first = *cfg;
+        first.narrow.no_zero_toi = 0;
+        validate_pipeline_cfg(first);
+        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
+        ccd_step(c, first, 0, 1, *report, nullptr);
+        if (report->toi != 0.0)
+            return;
+        ccdk_pipeline_cfg retry = *cfg;
+        retry.narrow.no_zero_toi = 1;
+        retry.narrow.min_separation = 0.0;
+        retry.min_sep_mode = CCDK_MINSEP_ABSOLUTE;
+        ccdk_report second;
+        ccd_step(c, retry, 0, 1, second, nullptr);
+        second.toi = 0.8 * second.toi; // one IEEE RN multiply, as in pipeline.cpp:252
+        second.t_cb += report->t_cb;
+        second.t_bp += report->t_bp;
+        second.t_socd += report->t_socd;
+        second.t_np += report->t_np;
+        *report = second;
+    });
+}
+
+int ccdk_query_min_separations(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+                               uint64_t n, const ccdk_pipeline_cfg* cfg, double* out)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (!n)
+            return;
+        uint8_t* dk = grow<uint8_t>(c.tmp[0], n);
+        double* dp = grow<double>(c.tmp[1], 24 * n);
+        double* dout = grow<double>(c.tmp[2], n);
+        h2d(c, dk, kind, n);
+        h2d(c, dp, points, 192 * n);
+        launch_min_seps(c, dk, dp, n, *cfg, dout);
+        d2h(c, out, dout, 8 * n);
+        sync(c);
+    });
+}
+
 int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr)
 {
     return guard(ctx, [&] { *dev_ptr = grow<double>(ctx->last_toi, 1); });
@@ -1004,8 +1189,8 @@ int ccdk_fetch_query_results(ccdk_ctx* ctx, double* toi, uint8_t* flags)
         std::lock_guard<std::mutex> lk(ctx->mu);
         Ctx& c = *ctx;
         const uint64_t n = c.last_query_count;
-        d2h(c, toi, c.out_toi.p, 8 * n);
-        d2h(c, flags, c.out_flags.p, n);
+        d2h(c, toi, c.all_toi.p, 8 * n);
+        d2h(c, flags, c.all_flags.p, n);
         sync(c);
     });
 }

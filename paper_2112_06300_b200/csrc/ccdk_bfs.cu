@@ -619,6 +619,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     st.evaluations += host_sc->evaluations;
     st.split_actions += host_sc->split_actions;
     st.generations = std::max<uint64_t>(st.generations, host_sc->gen);
+    c.narrow_any_flags |= host_sc->any_flags;
     return true;
 }
 
@@ -645,6 +646,7 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     ccdk_narrow_stats st {};
     st.global_toi = INFINITY;
     c.narrow_launches = 0;
+    c.narrow_any_flags = 0;
     const uint64_t n = in.n;
     out.toi = grow<double>(c.out_toi, n);
     out.flags = grow<uint8_t>(c.out_flags, n);
@@ -683,6 +685,7 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     }
     out.stats = st;
     out.launches = c.narrow_launches;
+    out.any_flags = st.overflow ? 0 : c.narrow_any_flags;
 }
 
 void launch_inclusion(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,

@@ -658,6 +658,8 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         CCDK_LAUNCH_CHECK();
         read_ctr();
         n_pairs = host_ctr[0];
+        out.range_lo = host_ctr[4]; // the swept left range (shard slice)
+        out.range_hi = host_ctr[5];
         if (n_pairs <= c.pair_capacity)
             break;
         c.pair_capacity = n_pairs + n_pairs / 4;

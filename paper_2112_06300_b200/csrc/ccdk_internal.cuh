@@ -93,6 +93,23 @@ struct DevBuf {
         }
         return p;
     }
+    // grow-only, preserving the first `cap` bytes (stream-ordered copy)
+    void* ensure_keep(size_t bytes, cudaStream_t s)
+    {
+        if (bytes > cap) {
+            void* np = nullptr;
+            const size_t c = bytes + bytes / 2;
+            CCDK_CUDA_CHECK(cudaMalloc(&np, c));
+            if (p) {
+                CCDK_CUDA_CHECK(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, s));
+                CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+                cudaFree(p);
+            }
+            p = np;
+            cap = c;
+        }
+        return p;
+    }
     template <typename T>
     T* as() const
     {
@@ -173,6 +190,7 @@ void launch_soa_to_aos(Ctx& c, const float* bmin, const float* bmax, uint64_t k,
 struct BroadOut {
     uint64_t n_pairs = 0;     // candidates (canonical, unique)
     uint64_t pair_tests = 0;
+    uint64_t range_lo = 0, range_hi = 0; // sorted left positions actually swept
     int axis = 0;
     float ms_axis_sort = 0, ms_sweep = 0, ms_pairsort = 0;
 };
@@ -206,6 +224,7 @@ struct NarrowOut {
     double* toi = nullptr;     // device, n (owned by ctx)
     uint8_t* flags = nullptr;  // device, n
     uint64_t launches = 0;     // generation + finish kernels launched
+    uint64_t any_flags = 0;    // OR of the per-query flags
 };
 void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out);
 void launch_inclusion(Ctx& c, const uint8_t* kind, const double* pts, const double* boxes,
@@ -219,6 +238,10 @@ void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
                           const double* v0, const double* v1, uint64_t nv,
                           const uint32_t* e, uint64_t ne, const uint32_t* f, uint8_t* kind,
                           double* pts);
+// query_min_separations (pipeline.cpp:39-55) incl. the distances of
+// distance.cpp (ccdk_distance.cu)
+void launch_min_seps(Ctx& c, const uint8_t* kind, const double* pts, uint64_t n,
+                     const ccdk_pipeline_cfg& cfg, double* out);
 void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
                         const uint8_t* own_kind, const uint32_t* own_index, uint64_t nv,
                         uint64_t ne, uint64_t* ids);
@@ -260,6 +283,10 @@ struct Ctx {
     DevBuf nscal;                      // NarrowScalars
     uint64_t last_query_count = 0;
     uint64_t narrow_launches = 0;
+    uint64_t narrow_any_flags = 0;
+    // pipeline results across batches
+    DevBuf all_keys, all_toi, all_flags;
+    bool last_keys_all = false; // fetch_pairs reads all_keys (pipeline) or pair_keys_sorted (API)
 
     // staging for API calls
     DevBuf tmp[8];

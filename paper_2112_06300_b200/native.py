@@ -66,6 +66,10 @@ _SIGS = {
                                     C.POINTER(abi.NarrowStats)]),
     "ccdk_ccd": (C.c_int, [C.c_void_p, P_F64, P_F64, C.c_uint64, P_U32, C.c_uint64, P_U32,
                            C.c_uint64, C.POINTER(abi.PipelineCfg), C.POINTER(abi.Report)]),
+    "ccdk_ccd_no_zero_toi": (C.c_int, [C.c_void_p, P_F64, P_F64, C.c_uint64, P_U32, C.c_uint64, P_U32,
+                                       C.c_uint64, C.POINTER(abi.PipelineCfg), C.POINTER(abi.Report)]),
+    "ccdk_query_min_separations": (C.c_int, [C.c_void_p, P_U8, P_F64, C.c_uint64,
+                                             C.POINTER(abi.PipelineCfg), P_F64]),
     "ccdk_scene_upload": (C.c_int, [C.c_void_p, P_F64, P_F64, C.c_uint64, P_U32, C.c_uint64, P_U32,
                                     C.c_uint64]),
     "ccdk_ccd_resident": (C.c_int, [C.c_void_p, C.POINTER(abi.PipelineCfg), C.c_uint32, C.c_uint32,

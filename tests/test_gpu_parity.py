@@ -342,3 +342,88 @@ def test_resident_step_shards_union(ctx, ref):
     # determinism across repeated device runs
     again = rs.step(cfg)
     assert again.toi.toi == full.toi.toi and again.candidate_count == full.candidate_count
+
+
+# ------------------------------------------------- batching, min-sep, retry
+
+def test_batching_transparency_matches_reference(ctx, ref):
+    """test_pipeline.cpp:68-87 / acceptance criterion 6: same ToI and
+    candidates at every budget; batch counts and tracked bytes equal the
+    reference's."""
+    s = scenes.make_box_soup(30, 4.0, 0.4, 1.0, 5)
+    full = ck.ccd(s, PipelineConfig(), ctx=ctx)
+    assert full.batch_count == 1
+    last = 1
+    for budget in [1 << 22, 1 << 20, 1 << 18, 1 << 16]:
+        cfg = PipelineConfig(memory_budget=budget)
+        got = ck.ccd(s, cfg, ctx=ctx)
+        exp, pairs = ref.ccd(s, cfg.to_c())
+        assert got.toi.toi == full.toi.toi == exp.toi
+        np.testing.assert_array_equal(got.candidates, full.candidates)
+        np.testing.assert_array_equal(got.candidates, pairs)
+        assert got.batch_count == exp.batch_count, budget
+        assert got.tracked_peak_bytes == exp.tracked_peak_bytes, budget
+        assert got.batch_count >= last
+        last = got.batch_count
+    assert last > 1
+    with pytest.raises(ck.ConfigError):
+        ck.ccd(plane_crossing_scene(), PipelineConfig(memory_budget=100), ctx=ctx)
+
+
+def test_query_min_separations_bit_exact(ctx, ref):
+    qb = concat(scenes.random_queries(2000, seed=51), scenes.degenerate_queries(40, seed=52))
+    cfg = PipelineConfig(min_sep_mode=ck.MINSEP_RELATIVE, min_sep_fraction=0.2)
+    got = ck.query_min_separations(qb, cfg, ctx)
+    exp = ref.query_min_separations(qb.kind, qb.points, cfg.to_c())
+    assert_bits(got, exp)
+    # plane-crossing scene: d0 = 1 -> 0.2 (test_pipeline.cpp:50-66)
+    q = plane_crossing_query()
+    assert ck.query_min_separations(q, cfg, ctx)[0] == 0.2 * 1.0
+    assert ck.point_triangle_distance([0.25, 0.25, 1], [0, 0, 0], [1, 0, 0], [0, 1, 0], ctx) == 1.0
+
+
+def test_relative_min_sep_pipeline(ctx, ref):
+    s = scenes.make_box_soup(40, 5.0, 0.4, 1.0, 1005)
+    cfg = PipelineConfig(min_sep_mode=ck.MINSEP_RELATIVE, inflation=0.01)
+    got = ck.ccd(s, cfg, ctx=ctx)
+    exp, pairs = ref.ccd(s, cfg.to_c())
+    assert got.toi.toi == exp.toi and got.toi.tolerance_hit == bool(exp.tolerance_hit)
+    np.testing.assert_array_equal(got.candidates, pairs)
+
+
+def test_zero_toi_retry(ctx, ref):
+    """test_pipeline.cpp:108-146: the 0.8 retry is bit-exact."""
+    s = plane_crossing_scene()
+    s.vertices_t0[3] = [0.25, 0.25, 1e-13]
+    s.vertices_t1[3] = [0.25, 0.25, -1.0]
+    cfg = PipelineConfig(narrow=NarrowConfig(no_zero_toi=True, min_separation=1e-6))
+    got = ck.ccd_no_zero_toi(s, cfg, ctx=ctx)
+    exp, _ = ref.ccd(s, cfg.to_c(), no_zero_retry=True)
+    assert got.toi.toi == exp.toi and got.toi.zero_toi_diagnostic == bool(exp.zero_toi_diagnostic)
+    assert got.toi.toi > 0.0 or got.toi.zero_toi_diagnostic
+    with pytest.raises(ck.ConfigError):
+        ck.ccd_no_zero_toi(s, PipelineConfig(), ctx=ctx)
+    # positive plain result: no retry
+    plain = ck.ccd_no_zero_toi(plane_crossing_scene(), PipelineConfig(narrow=NarrowConfig(no_zero_toi=True)), ctx=ctx)
+    assert plain.toi.toi == ck.ccd(plane_crossing_scene(), ctx=ctx).toi.toi > 0
+    # near-touching non-intersecting pair, Relative separation
+    s2 = plane_crossing_scene()
+    s2.vertices_t0[3] = [0.3, 0.3, 1e-8]
+    s2.vertices_t1[3] = [0.3, 0.3, -1e-4]
+    cfg2 = PipelineConfig(narrow=NarrowConfig(no_zero_toi=True), min_sep_mode=ck.MINSEP_RELATIVE)
+    r2 = ck.ccd_no_zero_toi(s2, cfg2, ctx=ctx)
+    e2, _ = ref.ccd(s2, cfg2.to_c(), no_zero_retry=True)
+    assert r2.toi.toi == e2.toi and r2.toi.toi > 0.0
+
+
+def test_query_results_fetch(ctx, ref):
+    s = scenes.make_cloth_scene(20, 20, 0.02, 1.0, 7)
+    cfg = PipelineConfig(inflation=0.01, memory_budget=1 << 19)
+    rs = ck.ResidentScene(s, ctx)
+    rep = rs.step(cfg)
+    toi, flags = rs.query_results(rep.query_count)
+    pairs = rs.candidates(rep.candidate_count)
+    cls = ref.classify(pairs, s)
+    etoi, eflags, _ = ref.narrow_phase(cls[0], cls[1], NarrowConfig().to_c())
+    assert_bits(toi, etoi)
+    np.testing.assert_array_equal(flags, eflags)
