@@ -130,6 +130,7 @@ typedef struct {
     int32_t reserved2;
     double ms_build, ms_sort, ms_sweep, ms_pairsort, ms_classify, ms_narrow, ms_total;
     uint64_t kernel_launches; /* own (non-CUB) kernels launched by this step */
+    uint64_t broad_batches;   /* BatchTrace::broad_batches */
 } ccdk_report;
 
 typedef struct ccdk_ctx ccdk_ctx;

@@ -618,6 +618,7 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     rep.ms_narrow = run.ms_narrow;
     rep.ms_total = ms_total;
     rep.kernel_launches = 1 + run.launches;
+    rep.broad_batches = run.broad_batches;
     rep.t_cb = ms_build * 1e-3;
     rep.t_bp = (run.ms_sort + run.ms_sweep + run.ms_pairsort) * 1e-3;
     rep.t_socd = run.ms_classify * 1e-3;
