@@ -1,0 +1,93 @@
+"""Multi-GPU host logic on CPU: world_size 2 over gloo.
+
+Each rank sweeps its equal-work slice of sorted left positions (the device
+partition rule, restated in multigpu.shard_bounds), runs classify + narrow on
+its own candidates with the CPU checker standing in for the device, and the
+ranks combine the ToI with the single allreduce(min).  The union of the
+shards' candidate sets must equal the single-process set, and the reduced ToI
+the single-process ToI (the SweepRange contract, broadphase.hpp:37-43).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2112_06300_b200 import abi, scenes
+from paper_2112_06300_b200.multigpu import shard_bounds, sorted_run_lengths
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2112_06300_b200.multigpu import allreduce_min_toi
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = oracle.orc()
+    s = scenes.make_cloth_scene(24, 24, 0.02, 1.0, 4)
+    boxes = orc.build_boxes(s, 0.01)
+    k = len(boxes[0])
+    axis = orc.choose_axis(boxes[0], boxes[1])
+    _, run_len = sorted_run_lengths(boxes[0], boxes[1], axis)
+    lo, hi = shard_bounds(run_len, 0, k - 1, rank, world)
+    pairs, _, _ = orc.broad(abi.BROAD_STQ, boxes, s, lo, hi)
+    kind, pts, _, _ = orc.classify(pairs, s)
+    toi = np.inf
+    if len(kind):
+        t, _, st = orc.narrow_phase(kind, pts, abi.narrow_cfg())
+        toi = st.global_toi
+    tt = torch.tensor([toi], dtype=torch.float64)
+    allreduce_min_toi(tt)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([len(pairs)], dtype=torch.int64))
+    mx = int(max(x.item() for x in sizes))
+    buf = torch.zeros((mx, 2), dtype=torch.int64)
+    buf[:len(pairs)] = torch.from_numpy(pairs.astype(np.int64))
+    gathered = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(gathered, buf)
+    if rank == 0:
+        union = np.concatenate([g[:int(n.item())].numpy() for g, n in zip(gathered, sizes)]).astype(np.uint64)
+        np.savez(result_path, union=union, toi=tt.numpy(), work=np.array([int(run_len[lo:hi].sum())]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_step_union_and_min_toi(tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+    world = 2
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    res = np.load(out)
+    s = scenes.make_cloth_scene(24, 24, 0.02, 1.0, 4)
+    rep, pairs = oracle.orc().ccd(s, abi.pipeline_cfg(inflation=0.01))
+    union = res["union"]
+    union = union[np.lexsort((union[:, 1], union[:, 0]))]
+    np.testing.assert_array_equal(union, pairs)
+    assert res["toi"][0] == rep.toi
+
+
+@pytest.mark.parametrize("count", [1, 2, 3, 8])
+def test_shard_bounds_partition(count):
+    rng = np.random.default_rng(5)
+    run_len = rng.integers(0, 50, size=1000).astype(np.uint64)
+    run_len[[3, 500]] = 100000  # heavy rows
+    bounds = [shard_bounds(run_len, 10, 990, r, count) for r in range(count)]
+    assert bounds[0][0] == 10 and bounds[-1][1] == 990
+    for a, b in zip(bounds, bounds[1:]):
+        assert a[1] == b[0]
+    total = int(run_len[10:990].sum())
+    for lo, hi in bounds:  # every shard's work is within one row of the ideal share
+        assert int(run_len[lo:hi].sum()) <= total / count + int(run_len.max())
