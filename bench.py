@@ -18,7 +18,6 @@ import argparse
 import json
 import os
 import platform
-import subprocess
 import sys
 import threading
 import time
@@ -39,7 +38,7 @@ WORKLOADS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
@@ -56,61 +55,74 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region through
+    in-process NVML (initialised before the timed region, so sampling is one
+    cheap driver query every `period` s; spawning nvidia-smi inside the timed
+    region stalls the driver and was measured to distort the step time)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.02):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period
+        self.samples = []
+        self.sm_max = None
+        self.nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.sm_max = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.nv = nv
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((sm, r))
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.stop.wait(self.period)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.nv is not None:
+            self.stop = threading.Event()
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self.nv is not None:
+            self.stop.set()
+            self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": [], "samples": 0,
+                    "source": "nvml" if self.nv else "unavailable"}
+        sm = sorted(s for s, _ in self.samples)
+        reasons = set()
+        for _, r in self.samples:
+            for name, const in self.REASONS:
+                bit = getattr(self.nv, const, 0)
+                if bit and (r & bit):
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.sm_max, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml"}
 
 
 def load_peaks():
@@ -193,6 +205,7 @@ def run_ours(args):
     scene = scenes.config_scene(args.workload)
     cfg = ck.PipelineConfig(inflation=0.01)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    clocks = ClockSampler(local)  # NVML initialised outside the timed region
 
     def barrier():
         if world > 1:
@@ -205,7 +218,6 @@ def run_ours(args):
             flush.zero_()
             rep = sharded.step(cfg)
         # ---- device-timed region: K full steps, L2 flushed before each
-        clocks = ClockSampler(local)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         barrier()
@@ -335,6 +347,7 @@ def run_ours(args):
         "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": int(d["kernel_launches"]) * args.steps,
         "wall_s_timed_region": wall,
+        "step_ms": [round(x, 3) for x in dev_ms],
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -17,6 +17,9 @@
 // three bisection depths packed in a u64; hi = lo + 2^-depth exactly.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstring>
+
 #include "ccdk_internal.cuh"
 #include "ccdk_interval.cuh"
 
@@ -51,6 +54,7 @@ struct GenArgs {
     unsigned long long phys_cap;
     unsigned long long sem_cap;
     NarrowScalars* sc;
+    cudaGraphConditionalHandle cond; // WHILE node of the generation graph
 };
 
 __device__ __forceinline__ unsigned long long dbits(double x)
@@ -277,8 +281,11 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
 __global__ void k_finish(GenArgs a)
 {
     NarrowScalars* sc = a.sc;
-    if (!sc->cont)
+    if (!sc->cont) {
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            cudaGraphSetConditional(a.cond, 0u);
         return;
+    }
     const unsigned long long nd = sc->dirty_n;
     for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < nd;
          i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
@@ -310,7 +317,14 @@ __global__ void k_finish(GenArgs a)
     sc->dropped = 0;
     sc->finish_ticket = 0;
     sc->cont = (raw_next > 0 && !sc->sem_overflow && !sc->phys_overflow) ? 1 : 0;
+    // a BFS tree is at most 3 x 1075 bisections deep; more generations than
+    // that means corrupted state, never a legitimate run
+    if (sc->cont && sc->gen > 4000) {
+        sc->cont = 0;
+        sc->gen_limit = 1;
+    }
     __threadfence();
+    cudaGraphSetConditional(a.cond, sc->cont ? 1u : 0u);
 }
 
 __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const double* pts,
@@ -512,6 +526,58 @@ T* grow(DevBuf& b, uint64_t n)
     return static_cast<T*>(b.ensure(n * sizeof(T)));
 }
 
+// Build (or reuse) the generation graph: WHILE(cond) { k_generation; k_finish }.
+// The condition defaults to 1 at every launch; k_finish clears it.
+void launch_generations(Ctx& c, GenArgs& a, unsigned gen_grid, unsigned fin_grid)
+{
+    GenGraph& G = c.gen_graph;
+    struct Key {
+        GenArgs a;
+        unsigned gen_grid, fin_grid;
+    } key;
+    std::memset(&key, 0, sizeof key);
+    key.a = a;
+    key.a.cond = 0;
+    key.gen_grid = gen_grid;
+    key.fin_grid = fin_grid;
+    static_assert(sizeof(Key) <= sizeof(G.key), "graph key too large");
+    if (G.exec && G.key_size == sizeof key && std::memcmp(G.key, &key, sizeof key) == 0) {
+        CCDK_CUDA_CHECK(cudaGraphLaunch(G.exec, c.stream));
+        return;
+    }
+    G.reset();
+    CCDK_CUDA_CHECK(cudaGraphCreate(&G.graph, 0));
+    cudaGraphConditionalHandle h;
+    CCDK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, G.graph, 1, cudaGraphCondAssignDefault));
+    a.cond = h;
+    cudaGraphNodeParams cp {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CCDK_CUDA_CHECK(cudaGraphAddNode(&cnode, G.graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    void* params[] = { &a };
+    cudaKernelNodeParams kp {};
+    kp.func = reinterpret_cast<void*>(k_generation);
+    kp.gridDim = dim3(gen_grid);
+    kp.blockDim = dim3(kGenBlock);
+    kp.sharedMemBytes = kGenSmem;
+    kp.kernelParams = params;
+    cudaGraphNode_t gnode, fnode;
+    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnode, body, nullptr, 0, &kp));
+    kp.func = reinterpret_cast<void*>(k_finish);
+    kp.gridDim = dim3(fin_grid);
+    kp.blockDim = dim3(256);
+    kp.sharedMemBytes = 0;
+    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, &gnode, 1, &kp));
+    CCDK_CUDA_CHECK(cudaGraphInstantiate(&G.exec, G.graph, 0));
+    std::memcpy(G.key, &key, sizeof key);
+    G.key_size = sizeof key;
+    CCDK_CUDA_CHECK(cudaGraphLaunch(G.exec, c.stream));
+}
+
 // One device run over queries [0, n) of `in`; returns false on physical
 // interval-buffer overflow (caller halves).
 bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const double* pts,
@@ -566,43 +632,29 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         a.v[0], a.dep[0]);
     CCDK_LAUNCH_CHECK();
 
-    int blocks_per_sm = 0;
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (c.gen_blocks_per_sm == 0) {
         CCDK_CUDA_CHECK(cudaFuncSetAttribute(k_generation, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenSmem));
         CCDK_CUDA_CHECK(cudaFuncSetAttribute(k_generation, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attr_set = true;
+        CCDK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.gen_blocks_per_sm, k_generation,
+                                                                      kGenBlock, kGenSmem));
+        c.gen_blocks_per_sm = std::max(1, c.gen_blocks_per_sm);
     }
-    CCDK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_generation,
-                                                                  kGenBlock, kGenSmem));
-    const unsigned gen_grid = static_cast<unsigned>(std::max(1, blocks_per_sm) * c.num_sms);
+    const unsigned gen_grid = static_cast<unsigned>(c.gen_blocks_per_sm * c.num_sms);
     const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
 
+    launch_generations(c, a, gen_grid, fin_grid);
+    c.narrow_launches += 2; // counted below from the generation count
+
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
-    const int batch = 8;
-    static const bool debug = getenv("CCDK_DEBUG") != nullptr;
-    for (;;) {
-        for (int g = 0; g < batch; ++g) {
-            k_generation<<<gen_grid, kGenBlock, kGenSmem, s>>>(a);
-            k_finish<<<fin_grid, 256, 0, s>>>(a);
-        }
-        c.narrow_launches += 2 * batch;
-        CCDK_LAUNCH_CHECK();
-        CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars),
-                                        cudaMemcpyDeviceToHost, s));
-        CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
-        if (debug)
-            fprintf(stderr, "[ccdk narrow] n=%llu gen=%llu cur=%llu peak=%llu evals=%llu splits=%llu cont=%llu phys=%llu sem=%llu\n",
-                    (unsigned long long)n, host_sc->gen, host_sc->cur_n, host_sc->peak,
-                    host_sc->evaluations, host_sc->split_actions, host_sc->cont,
-                    host_sc->phys_overflow, host_sc->sem_overflow);
-        if (!host_sc->cont)
-            break;
-        // a BFS tree is at most 3 x 1075 bisections deep; more generations
-        // than that means corrupted state, never a legitimate run
-        if (host_sc->gen > 4000)
-            throw Error(CCDK_CUDA, "narrow phase: generation limit exceeded (internal error)");
-    }
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
+    CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+    c.narrow_launches += 2 * host_sc->gen - 2;
+    if (debug_enabled())
+        fprintf(stderr, "[ccdk narrow] n=%llu gen=%llu peak=%llu evals=%llu splits=%llu phys=%llu sem=%llu\n",
+                (unsigned long long)n, host_sc->gen, host_sc->peak, host_sc->evaluations,
+                host_sc->split_actions, host_sc->phys_overflow, host_sc->sem_overflow);
+    if (host_sc->gen_limit)
+        throw Error(CCDK_CUDA, "narrow phase: generation limit exceeded (internal error)");
     if (host_sc->phys_overflow)
         return false;
     k_outputs<<<std::min<unsigned>(ig.x, 4096u), 256, 0, s>>>(n, a.toi, a.splits, a.exh_gen,

@@ -172,6 +172,32 @@ struct NarrowScalars {
     unsigned long long global_toi_bits;
     unsigned long long any_flags;   // OR of per-query flags
     unsigned long long vf_count;
+    unsigned long long gen_limit;   // set when the generation guard trips
+};
+
+// The narrow phase's generation loop as one CUDA graph: a WHILE conditional
+// node whose body is k_generation -> k_finish; k_finish clears the condition
+// when no further generation is needed, so the whole BFS runs without a host
+// round trip.  Re-instantiated only when the kernel arguments change.
+struct GenGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    unsigned char key[512];
+    size_t key_size = 0;
+    GenGraph() = default;
+    GenGraph(const GenGraph&) = delete;
+    GenGraph& operator=(const GenGraph&) = delete;
+    ~GenGraph() { reset(); }
+    void reset()
+    {
+        if (exec)
+            cudaGraphExecDestroy(exec);
+        if (graph)
+            cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        key_size = 0;
+    }
 };
 
 struct Ctx;
@@ -281,6 +307,8 @@ struct Ctx {
     DevBuf iv_qid[2], iv_t[2], iv_u[2], iv_v[2], iv_dep[2];
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
     DevBuf nscal;                      // NarrowScalars
+    GenGraph gen_graph;
+    int gen_blocks_per_sm = 0;
     uint64_t last_query_count = 0;
     uint64_t narrow_launches = 0;
     uint64_t narrow_any_flags = 0;
