@@ -38,7 +38,7 @@ WORKLOADS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
@@ -66,29 +66,37 @@ class ClockSampler:
                ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
                ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int, period: float = 0.02):
+    def __init__(self, index: int, period: float | None = None):
         self.index = index
-        self.period = period
+        self.period = period if period is not None else float(os.environ.get("BENCH_CLOCK_PERIOD", "0.1"))
         self.samples = []
         self.sm_max = None
         self.nv = None
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
         try:
             import pynvml as nv
             nv.nvmlInit()
             self.h = nv.nvmlDeviceGetHandleByIndex(index)
             self.sm_max = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
             self.nv = nv
+            for _ in range(3):  # first queries are slow (driver-side setup): keep them out
+                self._sample()
+            self.samples.clear()
+            self.call_ms = 0.0
         except Exception:
             self.nv = None
 
     def _sample(self):
         nv = self.nv
+        t0 = time.perf_counter()
         sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
         try:
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         except Exception:
             r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
         self.samples.append((sm, r))
+        self.call_ms = max(getattr(self, "call_ms", 0.0), (time.perf_counter() - t0) * 1e3)
 
     def _run(self):
         while not self.stop.is_set():
@@ -122,7 +130,8 @@ class ClockSampler:
                 if bit and (r & bit):
                     reasons.add(name)
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.sm_max, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml"}
+                "samples": len(sm), "source": "nvml", "period_s": self.period,
+                "max_query_ms": round(getattr(self, "call_ms", 0.0), 3)}
 
 
 def load_peaks():

@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ccdk_internal.cuh"
@@ -32,7 +33,7 @@ constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr int kGenBlock = 128;
 
 struct GenArgs {
-    uint8_t* qf;       // per-query kind | exact-widening flag (iv::kKind*)
+    uint32_t* qf;      // per-query kind | exact-widening flag (iv::kKind*)
     const uint8_t* kind;
     const double* pts;
     const double* sep;
@@ -44,8 +45,9 @@ struct GenArgs {
     unsigned long long* splits;
     unsigned* exh_gen;
     uint8_t* zdiag;
-    unsigned* dirty;
-    unsigned* dirty_mark;
+    unsigned* dirty;                 // queries whose ToI dropped (duplicates allowed)
+    unsigned long long dirty_cap;    // beyond it k_finish refreshes every query
+    unsigned long long nq;           // queries in this run
     uint32_t* qid[2];
     double* t[2];
     double* u[2];
@@ -55,6 +57,7 @@ struct GenArgs {
     unsigned long long sem_cap;
     NarrowScalars* sc;
     cudaGraphConditionalHandle cond; // WHILE node of the generation graph
+    unsigned zero;                   // always 0 (see atom_add_u64)
 };
 
 __device__ __forceinline__ unsigned long long dbits(double x)
@@ -78,37 +81,119 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Per-warp smem stage: 24 coordinates x 32 lanes, transposed (element-major)
-// so a warp reading element e touches 32 consecutive doubles.
+// Per-warp smem stages, element-major (element e of lane l at [32 e + l]) so
+// a warp reading element e touches 32 consecutive doubles:
+//   coordinates: 24 doubles per lane, double-buffered (batch b is evaluated
+//                from one buffer while batch b+W streams into the other);
+//   metadata:    the interval record (t, u, v lo, depths) and the per-query
+//                scalars (snapshot ToI, separation, exhausted generation |
+//                query flags), single-buffered: it is read into registers
+//                before the next batch's copy is issued.
+// Everything a batch needs arrives by cp.async, so no register load is in
+// flight across the evaluation (a register prefetch ties up scoreboards and
+// was measured to stall the loop head on the L2 round trip).
 constexpr int kStageDoubles = 24 * 32;
-constexpr int kGenSmem = (kGenBlock / 32) * 2 * kStageDoubles * sizeof(double);
+constexpr int kMetaDoubles = 7 * 32;
+constexpr int kQidDoubles = 16; // 32 query ids (u32) of batch b+W
+constexpr int kWarpSmemDoubles = 2 * kStageDoubles + kMetaDoubles + kQidDoubles;
+constexpr int kGenSmem = (kGenBlock / 32) * kWarpSmemDoubles * sizeof(double);
+enum { kMT = 0, kMU, kMV, kMDep, kMSnap, kMSep, kMExh };
 
-struct Prefetch {
-    unsigned q;
-    double tlo, ulo, vlo;
-    unsigned long long dp;
-    unsigned exh;
-    unsigned long long snap;
-    double sep;
-    uint8_t qf;
-    bool valid;
-};
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 
-__device__ __forceinline__ void stage_coords(const GenArgs& a, double* stage, unsigned lane, unsigned q)
+// Issue batch bb's copies: lane's interval i (if valid) of query q.
+__device__ __forceinline__ void stage_batch(const GenArgs& a, int cb, double* coords, double* meta,
+                                            unsigned lane, unsigned long long i, unsigned q)
 {
     const double* src = a.pts + 24ull * q;
 #pragma unroll
     for (int e = 0; e < 24; ++e)
-        cp_async8(stage + 32 * e + lane, src + e);
+        cp_async8(coords + 32 * e + lane, src + e);
+    cp_async8(meta + 32 * kMT + lane, a.t[cb] + i);
+    cp_async8(meta + 32 * kMU + lane, a.u[cb] + i);
+    cp_async8(meta + 32 * kMV + lane, a.v[cb] + i);
+    cp_async8(meta + 32 * kMDep + lane, a.dep[cb] + i);
+    cp_async8(meta + 32 * kMSnap + lane, a.snap + q);
+    if (a.sep)
+        cp_async8(meta + 32 * kMSep + lane, a.sep + q);
+    unsigned* ex = reinterpret_cast<unsigned*>(meta + 32 * kMExh + lane);
+    cp_async4(ex, a.exh_gen + q);
+    cp_async4(ex + 1, a.qf + q);
+}
+
+// Plain atomic add with the old value returned, on an address the compiler
+// cannot prove warp-uniform (callers offset it by `zero * lane`, zero a
+// runtime 0): ptxas rewrites uniform-address atomics into a warp-aggregated
+// form that broadcasts the result with a shuffle right after the atomic, i.e.
+// it would wait for the round trip that this kernel defers by a whole batch.
+__device__ __forceinline__ unsigned long long atom_add_u64(unsigned long long* p, unsigned long long v)
+{
+    unsigned long long old;
+    asm volatile("atom.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+
+// Children of an admitted split, written one batch after the split so the
+// append-cursor and split-budget atomics overlap the next evaluation.
+struct Pending {
+    unsigned long long slot_raw;   // leader's atomicAdd result (all lanes after shfl)
+    unsigned long long split_old;  // this lane's split-request counter before the request
+    unsigned long long dp;
+    double tlo, ulo, vlo;
+    unsigned long long dirty_slot; // dirty-list slot of a collision
+    unsigned q;
+    unsigned mask;                 // admit ballot of the batch
+    int dim;
+    int leader;
+    bool counted;                  // split_old holds a real request
+    bool collided;                 // this lane recorded a collision
+};
+
+__device__ __forceinline__ void finish_pending(const GenArgs& a, int nb, unsigned lane, unsigned gen,
+                                               const Pending& p)
+{
+    if (p.collided && p.dirty_slot < a.dirty_cap)
+        a.dirty[p.dirty_slot] = p.q;
+    if (!p.mask)
+        return;
+    const unsigned long long slot0 = __shfl_sync(0xffffffffu, p.slot_raw, p.leader);
+    if (p.mask & (1u << lane)) {
+        const unsigned long long s = slot0 + 2ull * __popc(p.mask & ((1u << lane) - 1));
+        if (s + 2 <= a.phys_cap) {
+            const unsigned dd = (p.dp >> (16 * p.dim)) & 0xffff;
+            const double lo = p.dim == 0 ? p.tlo : p.dim == 1 ? p.ulo : p.vlo;
+            // split_box (narrowphase.cpp:122-132): exact midpoint of a dyadic interval
+            const double mid = __dadd_rn(lo, __dmul_rn(0.5, iv::dyadic_width(dd)));
+            const unsigned long long dpc = p.dp + (1ull << (16 * p.dim));
+            a.qid[nb][s] = p.q;
+            a.qid[nb][s + 1] = p.q;
+            a.t[nb][s] = p.tlo;
+            a.t[nb][s + 1] = p.dim == 0 ? mid : p.tlo;
+            a.u[nb][s] = p.ulo;
+            a.u[nb][s + 1] = p.dim == 1 ? mid : p.ulo;
+            a.v[nb][s] = p.vlo;
+            a.v[nb][s + 1] = p.dim == 2 ? mid : p.vlo;
+            a.dep[nb][s] = dpc;
+            a.dep[nb][s + 1] = dpc;
+        } else {
+            a.sc->phys_overflow = 1;
+        }
+        if (p.counted && p.split_old >= a.max_splits)
+            a.exh_gen[p.q] = gen; // budget exhausted (narrowphase.cpp:263-271)
+    }
 }
 
 // One BFS generation: process_interval on every live interval + the fold
-// (narrowphase.cpp:226-305).  Each warp walks batches of 32 intervals with a
-// two-deep software pipeline: while batch b is evaluated from shared memory,
-// batch b+1's query coordinates stream in with cp.async and its interval
-// record and per-query scalars are already in flight into registers, and
-// batch b+2's query ids are being loaded.  The evaluation (~1.4k fp64/ALU
-// instructions per interval) hides all three latencies.
+// (narrowphase.cpp:226-305).  Each warp walks batches of 32 intervals
+// (stride W = number of warps) with a two-deep software pipeline: batch b is
+// evaluated from shared memory while batch b+W's coordinates and metadata
+// stream in by cp.async and batch b+2W's query ids load into a register; the
+// children of batch b are appended after batch b+W's evaluation (their
+// cursor atomic is issued at the end of batch b).
 __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
 {
     extern __shared__ double gsm[];
@@ -119,13 +204,10 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
     const unsigned gen = static_cast<unsigned>(sc->gen);
     const int cb = gen & 1, nb = cb ^ 1;
     const uint32_t* __restrict__ qid = a.qid[cb];
-    const double* __restrict__ ts = a.t[cb];
-    const double* __restrict__ us = a.u[cb];
-    const double* __restrict__ vs = a.v[cb];
-    const unsigned long long* __restrict__ ds = a.dep[cb];
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
-    double* stages = gsm + wib * 2 * kStageDoubles;
+    double* coords = gsm + wib * kWarpSmemDoubles;
+    double* meta = coords + 2 * kStageDoubles;
     const unsigned long long nbatch = (n + 31) >> 5;
     const unsigned long long W = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long b = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x >> 5) + wib;
@@ -133,55 +215,45 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
     if (b >= nbatch)
         return; // warp-uniform; no __syncthreads in this kernel
 
-    auto fetch = [&](unsigned long long bb, unsigned q, Prefetch& f) {
-        const unsigned long long i = (bb << 5) + lane;
-        f.valid = bb < nbatch && i < n;
-        if (f.valid) {
-            f.q = q;
-            f.tlo = ts[i];
-            f.ulo = us[i];
-            f.vlo = vs[i];
-            f.dp = ds[i];
-            f.exh = a.exh_gen[q];
-            f.snap = a.snap[q];
-            f.sep = a.sep ? a.sep[q] : a.sep_default;
-            f.qf = a.qf[q];
-        }
-    };
-    auto load_q = [&](unsigned long long bb) -> unsigned {
-        const unsigned long long i = (bb << 5) + lane;
-        return (bb < nbatch && i < n) ? qid[i] : 0u;
+    unsigned* qbuf = reinterpret_cast<unsigned*>(meta + kMetaDoubles);
+    auto in_range = [&](unsigned long long bb) { return bb < nbatch && (bb << 5) + lane < n; };
+    auto issue = [&](unsigned long long bb, unsigned q, int st) {
+        // batch bb's data (its query ids are known) and batch bb+W's query ids
+        if (in_range(bb))
+            stage_batch(a, cb, coords + st * kStageDoubles, meta, lane, (bb << 5) + lane, q);
+        if (in_range(bb + W))
+            cp_async4(qbuf + lane, qid + ((bb + W) << 5) + lane);
+        cp_async_commit();
     };
 
-    // prologue: batch b's coordinates + record, batch b+W's query id
-    Prefetch cur;
-    {
-        const unsigned q0 = load_q(b);
-        fetch(b, q0, cur);
-        if (cur.valid)
-            stage_coords(a, stages, lane, q0);
-        cp_async_commit();
-    }
-    unsigned q_next = load_q(b + W);
+    unsigned q_cur = in_range(b) ? qid[(b << 5) + lane] : 0u;
+    issue(b, q_cur, 0);
     int st = 0;
+    Pending pend;
+    pend.mask = 0;
 
     for (; b < nbatch; b += W) {
-        // issue batch b+W: coordinates into the other stage, record + scalars
-        Prefetch nxt;
-        fetch(b + W, q_next, nxt);
-        if (nxt.valid)
-            stage_coords(a, stages + (st ^ 1) * kStageDoubles, lane, q_next);
-        cp_async_commit();
-        q_next = load_q(b + 2 * W);
-        cp_async_wait<1>(); // batch b's copies (this lane's own) have landed
+        cp_async_wait<0>(); // batch b's coordinates + metadata, batch b+W's ids (issued one batch ago)
+        const unsigned long long i = (b << 5) + lane;
+        const bool valid = i < n;
+        const unsigned q = q_cur;
+        const double tlo = meta[32 * kMT + lane];
+        const double ulo = meta[32 * kMU + lane];
+        const double vlo = meta[32 * kMV + lane];
+        const unsigned long long dp = static_cast<unsigned long long>(__double_as_longlong(meta[32 * kMDep + lane]));
+        const unsigned long long snap = static_cast<unsigned long long>(__double_as_longlong(meta[32 * kMSnap + lane]));
+        const double sep = a.sep ? meta[32 * kMSep + lane] : a.sep_default;
+        const unsigned exh = reinterpret_cast<const unsigned*>(meta + 32 * kMExh + lane)[0];
+        const unsigned qf = reinterpret_cast<const unsigned*>(meta + 32 * kMExh + lane)[1];
+        q_cur = qbuf[lane];
+        // batch b+W: copies into the other coordinate buffer and the (now
+        // consumed) metadata stage; batch b+2W: query ids
+        issue(b + W, q_cur, st ^ 1);
 
-        bool admit = false;
+        bool admit = false, collided = false;
         int dim = -1;
-        unsigned long long split_old = 0;
-        if (cur.valid) {
-            const unsigned q = cur.q;
-            const double tlo = cur.tlo;
-            if (cur.exh < gen) {
+        if (valid) {
+            if (exh < gen) {
                 // exhausted in an earlier generation: fold t.lo and drop
                 // (narrowphase.cpp:280-291)
                 atomicMin(&a.toi[q], dbits(tlo));
@@ -189,87 +261,75 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
                     a.zdiag[q] = 1;
                 ++dropped;
             } else {
-                const unsigned long long dp = cur.dp;
                 iv::Box bx;
                 bx.tlo = tlo;
                 bx.thi = __dadd_rn(tlo, iv::dyadic_width(dp & 0xffff));
-                bx.ulo = cur.ulo;
-                bx.uhi = __dadd_rn(cur.ulo, iv::dyadic_width((dp >> 16) & 0xffff));
-                bx.vlo = cur.vlo;
-                bx.vhi = __dadd_rn(cur.vlo, iv::dyadic_width((dp >> 32) & 0xffff));
-                const double t_star = __longlong_as_double(static_cast<long long>(cur.snap));
-                const bool vf = !(cur.qf & iv::kKindEE);
-                const iv::SmemPts P { stages + st * kStageDoubles + lane };
+                bx.ulo = ulo;
+                bx.uhi = __dadd_rn(ulo, iv::dyadic_width((dp >> 16) & 0xffff));
+                bx.vlo = vlo;
+                bx.vhi = __dadd_rn(vlo, iv::dyadic_width((dp >> 32) & 0xffff));
+                const double t_star = __longlong_as_double(static_cast<long long>(snap));
+                const bool vf = !(qf & iv::kKindEE);
+                const iv::SmemPts P { coords + st * kStageDoubles + lane };
                 double cand = 0;
                 bool zd = false, evald = false;
                 int act;
-                if (!(cur.qf & iv::kKindExact))
-                    act = iv::process_one<iv::Fast>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
-                else
-                    act = iv::process_exact<iv::SmemPts>(vf, P, bx, t_star, cur.sep, a.cfg, cand, zd, dim, evald);
+                if (!(qf & iv::kKindExact))
+                    act = iv::process_one<iv::Fast>(vf, P, bx, t_star, sep, a.cfg, cand, zd, dim, evald);
+                else {
+                    const iv::Outcome o = iv::process_exact<iv::SmemPts>(vf, P, bx, t_star, sep, a.cfg);
+                    act = o.act;
+                    cand = o.cand;
+                    zd = o.zdiag;
+                    dim = o.dim;
+                    evald = o.evaluated;
+                }
                 evals += evald;
                 if (act == iv::kCollision) {
-                    const unsigned long long cbits = dbits(cand);
-                    const unsigned long long old = atomicMin(&a.toi[q], cbits);
-                    if (cbits < old && atomicExch(&a.dirty_mark[q], gen + 1) != gen + 1)
-                        a.dirty[atomicAdd(&sc->dirty_n, 1ull)] = q;
+                    // cand = t.lo < the snapshot (else the box was pruned), so
+                    // the query's ToI drops this generation: queue it for the
+                    // snapshot refresh (slot written one batch later)
+                    atomicMin(&a.toi[q], dbits(cand));
+                    collided = true;
                     if (zd)
                         a.zdiag[q] = 1;
                 } else if (act == iv::kSplit) {
-                    // Every split is appended; the request counter's old value
-                    // is consumed only after the append (its round trip
-                    // overlaps the cursor atomic).  A request beyond the
-                    // budget marks the query exhausted in this generation;
-                    // its children are then folded (min t.lo, zdiag at
-                    // t.lo == 0) and dropped at the start of the next one,
-                    // which equals the reference's fold of every split
-                    // interval of the exhausting generation
-                    // (narrowphase.cpp:254-297): a child's t.lo is >= its
-                    // parent's and the left child's equals it.
+                    // Every split is appended; a request beyond the budget
+                    // marks the query exhausted in this generation; its
+                    // children are then folded (min t.lo, zdiag at t.lo == 0)
+                    // and dropped at the start of the next one, which equals
+                    // the reference's fold of every split interval of the
+                    // exhausting generation (narrowphase.cpp:254-297): a
+                    // child's t.lo is >= its parent's and the left child's
+                    // equals it.
                     ++split_actions;
                     admit = true;
-                    if (!(a.cfg.no_zero_toi && tlo == 0.0))
-                        split_old = atomicAdd(&a.splits[q], 1ull);
                 }
             }
         }
-        // warp-aggregated append of the two children per admitted split
-        const unsigned mask = __ballot_sync(0xffffffffu, admit);
-        if (mask) {
-            unsigned long long slot0 = 0;
-            const int leader = __ffs(mask) - 1;
-            if (lane == static_cast<unsigned>(leader))
-                slot0 = atomicAdd(&sc->next_n, 2ull * __popc(mask));
-            slot0 = __shfl_sync(0xffffffffu, slot0, leader);
-            if (admit) {
-                const unsigned long long s = slot0 + 2ull * __popc(mask & ((1u << lane) - 1));
-                if (s + 2 <= a.phys_cap) {
-                    const unsigned long long dp = cur.dp;
-                    const unsigned dd = (dp >> (16 * dim)) & 0xffff;
-                    const double lo = dim == 0 ? cur.tlo : dim == 1 ? cur.ulo : cur.vlo;
-                    // split_box (narrowphase.cpp:122-132): exact midpoint
-                    const double mid = __dadd_rn(lo, __dmul_rn(0.5, iv::dyadic_width(dd)));
-                    const unsigned long long dpc = dp + (1ull << (16 * dim));
-                    a.qid[nb][s] = cur.q;
-                    a.qid[nb][s + 1] = cur.q;
-                    a.t[nb][s] = cur.tlo;
-                    a.t[nb][s + 1] = dim == 0 ? mid : cur.tlo;
-                    a.u[nb][s] = cur.ulo;
-                    a.u[nb][s + 1] = dim == 1 ? mid : cur.ulo;
-                    a.v[nb][s] = cur.vlo;
-                    a.v[nb][s + 1] = dim == 2 ? mid : cur.vlo;
-                    a.dep[nb][s] = dpc;
-                    a.dep[nb][s + 1] = dpc;
-                } else {
-                    sc->phys_overflow = 1;
-                }
-            }
-        }
-        if (split_old >= a.max_splits)
-            a.exh_gen[cur.q] = gen; // budget exhausted (narrowphase.cpp:263-271)
-        cur = nxt;
+        // children of the previous batch (their atomics have had a whole
+        // evaluation to return), then this batch's requests
+        finish_pending(a, nb, lane, gen, pend);
+        Pending np;
+        np.counted = admit && !(a.cfg.no_zero_toi && tlo == 0.0);
+        np.split_old = np.counted ? atom_add_u64(&a.splits[q], 1ull) : 0ull;
+        np.collided = collided;
+        np.dirty_slot = collided ? atom_add_u64(&sc->dirty_n + a.zero * lane, 1ull) : 0ull;
+        np.mask = __ballot_sync(0xffffffffu, admit);
+        np.leader = np.mask ? __ffs(np.mask) - 1 : 0;
+        np.slot_raw = 0;
+        if (np.mask && lane == static_cast<unsigned>(np.leader))
+            np.slot_raw = atom_add_u64(&sc->next_n + a.zero * lane, 2ull * __popc(np.mask));
+        np.dp = dp;
+        np.tlo = tlo;
+        np.ulo = ulo;
+        np.vlo = vlo;
+        np.q = q;
+        np.dim = dim;
+        pend = np;
         st ^= 1;
     }
+    finish_pending(a, nb, lane, gen, pend);
     cp_async_wait<0>();
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);
@@ -282,14 +342,16 @@ __global__ void k_finish(GenArgs a)
 {
     NarrowScalars* sc = a.sc;
     if (!sc->cont) {
-        if (blockIdx.x == 0 && threadIdx.x == 0)
+        if (blockIdx.x == 0 && threadIdx.x == 0 && a.cond)
             cudaGraphSetConditional(a.cond, 0u);
         return;
     }
     const unsigned long long nd = sc->dirty_n;
-    for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < nd;
+    const bool all = nd > a.dirty_cap; // list overflowed: refresh every query
+    const unsigned long long m = all ? a.nq : nd;
+    for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
-        const unsigned q = a.dirty[i];
+        const unsigned q = all ? static_cast<unsigned>(i) : a.dirty[i];
         a.snap[q] = a.toi[q];
     }
     __shared__ bool last;
@@ -324,13 +386,14 @@ __global__ void k_finish(GenArgs a)
         sc->gen_limit = 1;
     }
     __threadfence();
-    cudaGraphSetConditional(a.cond, sc->cont ? 1u : 0u);
+    if (a.cond)
+        cudaGraphSetConditional(a.cond, sc->cont ? 1u : 0u);
 }
 
 __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const double* pts,
-                               uint8_t* qf, unsigned long long* toi,
+                               uint32_t* qf, unsigned long long* toi,
                                unsigned long long* snap, unsigned long long* splits,
-                               unsigned* exh_gen, uint8_t* zdiag, unsigned* dirty_mark,
+                               unsigned* exh_gen, uint8_t* zdiag,
                                uint32_t* qid, double* t, double* u, double* v,
                                unsigned long long* dep)
 {
@@ -341,9 +404,8 @@ __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const 
         splits[q] = 0;
         exh_gen[q] = kNoGen;
         zdiag[q] = 0;
-        dirty_mark[q] = 0;
         qid[q] = static_cast<uint32_t>(q); // one root box [0,1]^3 per query
-        qf[q] = static_cast<uint8_t>((kind[q] == CCDK_QUERY_EE ? iv::kKindEE : 0)
+        qf[q] = static_cast<uint32_t>((kind[q] == CCDK_QUERY_EE ? iv::kKindEE : 0)
                                      | (iv::fast_ok(iv::GlobalPts { pts + 24 * q }) ? 0 : iv::kKindExact));
         t[q] = 0.0;
         u[q] = 0.0;
@@ -597,7 +659,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         return false;
     GenArgs a {};
     a.kind = kind;
-    a.qf = grow<uint8_t>(c.q_flags, n);
+    a.qf = grow<uint32_t>(c.q_flags, n);
     a.pts = pts;
     a.sep = sep;
     a.sep_default = in.cfg.min_separation;
@@ -609,7 +671,8 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     a.exh_gen = grow<unsigned>(c.exh_gen, n);
     a.zdiag = grow<uint8_t>(c.zdiag, n);
     a.dirty = grow<unsigned>(c.dirty, 2 * n);
-    a.dirty_mark = a.dirty + n;
+    a.dirty_cap = 2 * n;
+    a.nq = n;
     for (int b = 0; b < 2; ++b) {
         a.qid[b] = grow<uint32_t>(c.iv_qid[b], cap);
         a.t[b] = grow<double>(c.iv_t[b], cap);
@@ -628,7 +691,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, &init, sizeof init, cudaMemcpyHostToDevice, s));
     const dim3 ig = grid_for(n, 256);
     k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(
-        n, kind, pts, a.qf, a.toi, a.snap, a.splits, a.exh_gen, a.zdiag, a.dirty_mark, a.qid[0], a.t[0], a.u[0],
+        n, kind, pts, a.qf, a.toi, a.snap, a.splits, a.exh_gen, a.zdiag, a.qid[0], a.t[0], a.u[0],
         a.v[0], a.dep[0]);
     CCDK_LAUNCH_CHECK();
 
@@ -642,7 +705,26 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     const unsigned gen_grid = static_cast<unsigned>(c.gen_blocks_per_sm * c.num_sms);
     const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
 
-    launch_generations(c, a, gen_grid, fin_grid);
+    static const bool no_graph = std::getenv("CCDK_NO_GRAPH") != nullptr;
+    if (!no_graph) {
+        launch_generations(c, a, gen_grid, fin_grid);
+    } else {
+        // direct launches (profilers cannot see kernel nodes under a
+        // conditional node): batches of 8 generations, then a host check
+        a.cond = 0;
+        NarrowScalars* hs = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
+        for (;;) {
+            for (int g = 0; g < 8; ++g) {
+                k_generation<<<gen_grid, kGenBlock, kGenSmem, s>>>(a);
+                k_finish<<<fin_grid, 256, 0, s>>>(a);
+            }
+            CCDK_LAUNCH_CHECK();
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(hs, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
+            CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+            if (!hs->cont)
+                break;
+        }
+    }
     c.narrow_launches += 2; // counted below from the generation count
 
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));

@@ -289,12 +289,20 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 // magnitude (see the header comment).
 // The Exact-widening instantiation is out of line: it runs only for queries
 // beyond 2^1000 and would otherwise double the hot loop's code size.
+struct Outcome {
+    double cand;
+    int act, dim;
+    bool zdiag, evaluated;
+};
+
 template <class Pts>
-__device__ __noinline__ int process_exact(bool vf, const Pts P, const Box b, double t_star,
-                                          double d, const Cfg cfg, double& cand_t, bool& zdiag,
-                                          int& dim, bool& evaluated)
+__device__ __noinline__ Outcome process_exact(bool vf, const Pts P, const Box b, double t_star,
+                                              double d, const Cfg cfg)
 {
-    return process_one<Exact, Pts>(vf, P, b, t_star, d, cfg, cand_t, zdiag, dim, evaluated);
+    Outcome o;
+    o.cand = 0.0;
+    o.act = process_one<Exact, Pts>(vf, P, b, t_star, d, cfg, o.cand, o.zdiag, o.dim, o.evaluated);
+    return o;
 }
 
 template <class Pts>
