@@ -31,6 +31,9 @@ namespace {
 constexpr unsigned kNoGen = 0xffffffffu;
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr int kGenBlock = 128;
+#ifndef CCDK_GEN_MINB
+#define CCDK_GEN_MINB 4
+#endif
 
 struct GenArgs {
     uint32_t* qf;      // per-query kind | exact-widening flag (iv::kKind*)
@@ -95,7 +98,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int kStageDoubles = 24 * 32;
 constexpr int kMetaDoubles = 7 * 32;
 constexpr int kQidDoubles = 16; // 32 query ids (u32) of batch b+W
-constexpr int kWarpSmemDoubles = 2 * kStageDoubles + kMetaDoubles + kQidDoubles;
+#ifndef CCDK_GEN_STAGES
+#define CCDK_GEN_STAGES 1 // coordinate buffers per warp (1: the copy of batch b+W waits for b's evaluation)
+#endif
+constexpr int kStages = CCDK_GEN_STAGES;
+constexpr int kWarpSmemDoubles = kStages * kStageDoubles + kMetaDoubles + kQidDoubles;
 constexpr int kGenSmem = (kGenBlock / 32) * kWarpSmemDoubles * sizeof(double);
 enum { kMT = 0, kMU, kMV, kMDep, kMSnap, kMSep, kMExh };
 
@@ -194,7 +201,7 @@ __device__ __forceinline__ void finish_pending(const GenArgs& a, int nb, unsigne
 // stream in by cp.async and batch b+2W's query ids load into a register; the
 // children of batch b are appended after batch b+W's evaluation (their
 // cursor atomic is issued at the end of batch b).
-__global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
+__global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs a)
 {
     extern __shared__ double gsm[];
     NarrowScalars* sc = a.sc;
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
     double* coords = gsm + wib * kWarpSmemDoubles;
-    double* meta = coords + 2 * kStageDoubles;
+    double* meta = coords + kStages * kStageDoubles;
     const unsigned long long nbatch = (n + 31) >> 5;
     const unsigned long long W = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long b = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x >> 5) + wib;
@@ -229,8 +236,7 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
     unsigned q_cur = in_range(b) ? qid[(b << 5) + lane] : 0u;
     issue(b, q_cur, 0);
     int st = 0;
-    Pending pend;
-    pend.mask = 0;
+    Pending pend {}; // nothing pending before the first batch (mask 0, no collision)
 
     for (; b < nbatch; b += W) {
         cp_async_wait<0>(); // batch b's coordinates + metadata, batch b+W's ids (issued one batch ago)
@@ -248,7 +254,8 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
         q_cur = qbuf[lane];
         // batch b+W: copies into the other coordinate buffer and the (now
         // consumed) metadata stage; batch b+2W: query ids
-        issue(b + W, q_cur, st ^ 1);
+        if (kStages == 2)
+            issue(b + W, q_cur, st ^ 1);
 
         bool admit = false, collided = false;
         int dim = -1;
@@ -327,7 +334,12 @@ __global__ void __launch_bounds__(kGenBlock) k_generation(GenArgs a)
         np.q = q;
         np.dim = dim;
         pend = np;
-        st ^= 1;
+        if (kStages == 2) {
+            st ^= 1;
+        } else {
+            __syncwarp(); // every lane's evaluation has read the stage
+            issue(b + W, q_cur, 0);
+        }
     }
     finish_pending(a, nb, lane, gen, pend);
     cp_async_wait<0>();
@@ -716,7 +728,15 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         for (;;) {
             for (int g = 0; g < 8; ++g) {
                 k_generation<<<gen_grid, kGenBlock, kGenSmem, s>>>(a);
+                if (debug_enabled()) {
+                    const cudaError_t e = cudaStreamSynchronize(s);
+                    fprintf(stderr, "[ccdk narrow] k_generation: %s\n", cudaGetErrorString(e));
+                }
                 k_finish<<<fin_grid, 256, 0, s>>>(a);
+                if (debug_enabled()) {
+                    const cudaError_t e = cudaStreamSynchronize(s);
+                    fprintf(stderr, "[ccdk narrow] k_finish: %s\n", cudaGetErrorString(e));
+                }
             }
             CCDK_LAUNCH_CHECK();
             CCDK_CUDA_CHECK(cudaMemcpyAsync(hs, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));

@@ -14,7 +14,8 @@ import numpy as np
 from . import abi
 from .abi import P_F32, P_F64, P_U8, P_U16, P_U32, P_U64
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libccdk.so")
+LIB_PATH = os.environ.get("CCDK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                     "libccdk.so")
 
 
 class CcdkError(RuntimeError):
