@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--c5-queries", type=int, default=10_000_000,
+                    help="narrow-phase-only leg (BASELINE config 5); 0 disables")
+    ap.add_argument("--c5-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -194,6 +197,94 @@ def run_reference(args):
     return 0
 
 
+def narrow_only_leg(args, torch, ck, scenes, stream, flush, rank, world, local):
+    """BASELINE config 5: narrow phase only over 10M mixed VF/EE queries incl.
+    rotated near-degenerates and 16 budget-exhausting slides.  Queries are
+    sharded by count (contiguous blocks) across ranks; the global ToI is one
+    allreduce(min).  Device-timed with queries resident in HBM; e2e through
+    the C ABI from pinned host buffers (H2D of the queries, D2H of per-query
+    ToI + flags)."""
+    import numpy as np
+    dev = f"cuda:{local}"
+    n_all = args.c5_queries
+    qb = scenes.config_queries(n_all)
+    lo, hi = rank * n_all // world, (rank + 1) * n_all // world
+    n = hi - lo
+    kind_h = torch.from_numpy(np.ascontiguousarray(qb.kind[lo:hi])).pin_memory()
+    pts_h = torch.from_numpy(np.ascontiguousarray(qb.points[lo:hi])).pin_memory()
+    kind_d = kind_h.to(dev)
+    pts_d = pts_h.to(dev)
+    toi_d = torch.empty(n, dtype=torch.float64, device=dev)
+    flags_d = torch.empty(n, dtype=torch.uint8, device=dev)
+    gtoi = torch.full((1,), float("inf"), dtype=torch.float64, device=dev)
+
+    def run():
+        return ck.narrow_phase_device(kind_d.data_ptr(), pts_d.data_ptr(), n, toi_ptr=toi_d.data_ptr(),
+                                      flags_ptr=flags_d.data_ptr())
+
+    with torch.cuda.stream(stream):
+        out = run()  # warm-up
+        evs = []
+        for _ in range(args.c5_steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out = run()
+            gtoi.fill_(out.global_toi)
+            if world > 1:
+                torch.distributed.all_reduce(gtoi, op=torch.distributed.ReduceOp.MIN)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+        # e2e: host queries -> C ABI -> host per-query results
+        e2e_ms = None
+        if not args.no_e2e:
+            hq = scenes.QueryBatch(kind_h.numpy(), pts_h.numpy())
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            res = ck.narrow_phase(hq)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = a.elapsed_time(b)
+    vals = torch.tensor([ms, e2e_ms or 0.0], dtype=torch.float64, device=dev)
+    work = torch.tensor([out.evaluations, out.split_actions, out.total_splits], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(work, op=torch.distributed.ReduceOp.SUM)
+    ms, e2e_ms = vals.tolist()[0], (vals.tolist()[1] or None)
+    evals, splits, total_splits = (int(x) for x in work.tolist())
+    leg = {"workload": "C5", "queries": n_all, "data": scenes.CONFIGS["C5"],
+           "ms": ms, "queries_per_s": n_all / (ms * 1e-3),
+           "global_toi": float(gtoi.item()), "evaluations": evals, "split_actions": splits,
+           "total_splits": total_splits, "generations_rank0": out.generations,
+           "sharding": f"contiguous query blocks x{world}, allreduce(min)",
+           "e2e": None if e2e_ms is None else {
+               "value": n_all / (e2e_ms * 1e-3), "unit": "queries/s", "ms": e2e_ms,
+               "h2d_bytes_per_step": int(kind_h.numel() + pts_h.numel() * 8) * world,
+               "d2h_bytes_per_step": 9 * n_all}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            if oracle.ref_available():
+                threads = os.cpu_count() or 1
+                m = min(50_000, n_all)
+                import time as _t
+                t0 = _t.perf_counter()
+                ctoi, cfl, cst = oracle.ref(threads).narrow_phase(qb.kind[:m], qb.points[:m],
+                                                                  ck.NarrowConfig().to_c())
+                cpu_s = _t.perf_counter() - t0
+                leg["cpu_baseline"] = {
+                    "value": m / cpu_s, "unit": "queries/s", "cores": threads, "kind": "reference",
+                    "sample": f"first {m} C5 queries (incl. {m // 10000} rotated near-degenerates, no "
+                              f"budget-exhausting ones) via ccdkit_ref::narrow_phase threads={threads}",
+                    "bit_exact_vs_gpu": bool(np.array_equal(ctoi.view(np.uint64), toi_d[:m].cpu().numpy().view(np.uint64))
+                                             and np.array_equal(cfl, flags_d[:m].cpu().numpy()))}
+        except Exception as e:
+            leg["cpu_baseline"] = {"error": str(e)}
+    return leg
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -287,6 +378,10 @@ def run_ours(args):
     ms, e2e_max, narrow_ms = vals.tolist()
     queries, candidates = (int(x) for x in counts.tolist())
 
+    c5 = None
+    if args.c5_queries > 0:
+        c5 = narrow_only_leg(args, torch, ck, scenes, stream, flush, rank, world, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -335,6 +430,13 @@ def run_ours(args):
                       "algorithmic": f"B = 40k + 8C, k={k}, C={rep.candidate_count}",
                       "pair_tests": d["pair_tests"],
                       "pair_tests_per_s": d["pair_tests"] / (d["ms_sweep"] * 1e-3) if d["ms_sweep"] else None}
+    if c5:
+        f5 = 339.0 * c5["evaluations"] + 96.0 * c5["split_actions"]
+        a5 = f5 / (c5["ms"] * 1e-3) / 1e12 / world
+        c5["roofline"] = {"kernel": "k_generation (C5 narrow phase, all generations)", "bound": "fp64",
+                          "achieved": a5, "peak": fp64_peak, "unit": "TFLOP/s", "frac": a5 / fp64_peak,
+                          "per": "GPU", "algorithmic": f"F = 339*E + 96*S, E={c5['evaluations']}, "
+                                                       f"S={c5['split_actions']}"}
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
@@ -357,6 +459,7 @@ def run_ours(args):
         "gpu_launches": int(d["kernel_launches"]) * args.steps,
         "wall_s_timed_region": wall,
         "step_ms": [round(x, 3) for x in dev_ms],
+        "narrow_only": c5,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

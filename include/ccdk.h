@@ -214,6 +214,16 @@ CCDK_API int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double*
                       const ccdk_narrow_cfg* cfg, uint64_t queue_capacity,
                       double* toi, uint8_t* flags, ccdk_narrow_stats* stats);
 
+/* narrow_phase on device-resident queries: kind/points/per_query_sep/toi/
+ * flags are DEVICE pointers (toi/flags may be NULL: results then stay in the
+ * context).  Same semantics and stats as ccdk_narrow_phase; used for the
+ * device-timed narrow-only benchmark (BASELINE config 5) and by multi-GPU
+ * hosts that shard queries on the device. */
+CCDK_API int ccdk_narrow_phase_device(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+                                      const double* per_query_sep, uint64_t n,
+                                      const ccdk_narrow_cfg* cfg, uint64_t queue_capacity,
+                                      double* toi, uint8_t* flags, ccdk_narrow_stats* stats);
+
 /* ---- pipeline: pipeline.hpp --------------------------------------------- */
 /* ccd (pipeline.hpp:67, pipeline.cpp:218-232): the full CCD step from host
  * buffers (H2D copy, box build, broad phase, classify, narrow phase, global

@@ -371,6 +371,24 @@ def narrow_phase(queries: QueryBatch, cfg: NarrowConfig | None = None, threads: 
                          int(st.split_actions), int(st.generations), float(st.device_ms))
 
 
+def narrow_phase_device(kind_ptr: int, points_ptr: int, n: int, cfg: NarrowConfig | None = None,
+                        toi_ptr: int | None = None, flags_ptr: int | None = None,
+                        sep_ptr: int | None = None, queue_capacity: int = abi.UINT64_MAX,
+                        ctx=None) -> NarrowOutcome:
+    """narrow_phase on device-resident queries (device pointers, e.g. from
+    torch tensors); per-query results go to toi_ptr/flags_ptr when given."""
+    cfg = cfg or NarrowConfig()
+    c = _ctx(ctx)
+    st = abi.NarrowStats()
+    ccfg = cfg.to_c()
+    vp = lambda x: None if x is None else C.c_void_p(int(x))
+    check(lib().ccdk_narrow_phase_device(c.h, vp(kind_ptr), vp(points_ptr), vp(sep_ptr), n, C.byref(ccfg),
+                                         queue_capacity, vp(toi_ptr), vp(flags_ptr), C.byref(st)))
+    return NarrowOutcome(None, None, st.global_toi, bool(st.overflow), int(st.peak_queue),
+                         int(st.total_splits), int(st.evaluations), int(st.split_actions),
+                         int(st.generations), float(st.device_ms))
+
+
 # -------------------------------------------------------------- pipeline.hpp
 
 def _report(r: abi.Report, pairs) -> CcdReport:

@@ -432,9 +432,7 @@ struct BatchRun {
         candidates += n;
         base_bytes = k * 32 + candidates * 16;
         // classify (K7) + query_min_separations
-        cudaEvent_t e0, e1;
-        CCDK_CUDA_CHECK(cudaEventCreate(&e0));
-        CCDK_CUDA_CHECK(cudaEventCreate(&e1));
+        cudaEvent_t e0 = c.events.get(EventPool::kBatch), e1 = c.events.get(EventPool::kBatch + 1);
         CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
         uint8_t* qk = grow<uint8_t>(c.q_kind, std::max<uint64_t>(n, 1));
         double* qp = grow<double>(c.q_points, 24 * std::max<uint64_t>(n, 1));
@@ -467,8 +465,6 @@ struct BatchRun {
         float ms = 0;
         CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
         ms_classify += ms;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
         vf += nvf;
     }
 
@@ -543,8 +539,8 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     if (cap_pairs < 1)
         throw Error(CCDK_CONFIG, "memory budget too small to hold even one query");
     cudaEvent_t ev[6];
-    for (auto& e : ev)
-        CCDK_CUDA_CHECK(cudaEventCreate(&e));
+    for (int i = 0; i < 6; ++i)
+        ev[i] = c.events.get(EventPool::kStep + i);
     CCDK_CUDA_CHECK(cudaEventRecord(ev[0], st));
 
     // K1 (the scene was validated when it was uploaded)
@@ -623,8 +619,6 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     rep.t_bp = (run.ms_sort + run.ms_sweep + run.ms_pairsort) * 1e-3;
     rep.t_socd = run.ms_classify * 1e-3;
     rep.t_np = run.ms_narrow * 1e-3;
-    for (auto& e : ev)
-        cudaEventDestroy(e);
 }
 
 } // namespace
@@ -1068,6 +1062,38 @@ int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
     });
 }
 
+int ccdk_narrow_phase_device(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
+                             const double* per_query_sep, uint64_t n, const ccdk_narrow_cfg* cfg,
+                             uint64_t queue_capacity, double* toi, uint8_t* flags,
+                             ccdk_narrow_stats* stats)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        validate_narrow_cfg(*cfg);
+        std::memset(stats, 0, sizeof *stats);
+        stats->global_toi = INFINITY;
+        if (!n)
+            return;
+        NarrowIn ni;
+        ni.kind = kind;
+        ni.points = points;
+        ni.sep = per_query_sep;
+        ni.n = n;
+        ni.cfg = *cfg;
+        ni.queue_capacity = queue_capacity;
+        NarrowOut no;
+        narrow_phase(c, ni, no);
+        if (toi)
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(toi, no.toi, 8 * n, cudaMemcpyDeviceToDevice, c.stream));
+        if (flags)
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(flags, no.flags, n, cudaMemcpyDeviceToDevice, c.stream));
+        sync(c);
+        *stats = no.stats;
+    });
+}
+
 int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
                       const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf)
 {
@@ -1106,12 +1132,10 @@ int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
             if (nv)
                 throw Error(CCDK_INVALID_INPUT, "vertex snapshots missing");
         }
-        cudaEvent_t start;
-        CCDK_CUDA_CHECK(cudaEventCreate(&start));
+        cudaEvent_t start = c.events.get(EventPool::kApi);
         CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
         upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
         ccd_step(c, *cfg, 0, 1, *report, start);
-        cudaEventDestroy(start);
     });
 }
 

@@ -660,11 +660,20 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     cudaStream_t s = c.stream;
     uint64_t cap = c.interval_capacity;
     if (cap == 0) {
-        size_t free_b = 0, total_b = 0;
-        CCDK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-        const uint64_t by_mem = static_cast<uint64_t>(free_b / 2) / 72;
+        // size from free memory, probed once per query count (cudaMemGetInfo
+        // is a slow driver query; keep it off the steady-state path)
+        if (c.mem_probe_n == 0 || n > c.mem_probe_n) {
+            size_t free_b = 0, total_b = 0;
+            CCDK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            // already-allocated interval buffers count as available
+            size_t held = 0;
+            for (int b = 0; b < 2; ++b)
+                held += c.iv_qid[b].cap + c.iv_t[b].cap + c.iv_u[b].cap + c.iv_v[b].cap + c.iv_dep[b].cap;
+            c.mem_probe_cap = static_cast<uint64_t>((free_b + held) / 2) / 72;
+            c.mem_probe_n = n;
+        }
         cap = std::max<uint64_t>(4 * n, uint64_t(1) << 24);
-        cap = std::min<uint64_t>(cap, by_mem);
+        cap = std::min<uint64_t>(cap, c.mem_probe_cap);
         cap = std::max<uint64_t>(cap, n);
     }
     if (cap < n)
@@ -804,9 +813,7 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     const uint64_t n = in.n;
     out.toi = grow<double>(c.out_toi, n);
     out.flags = grow<uint8_t>(c.out_flags, n);
-    cudaEvent_t e0, e1;
-    CCDK_CUDA_CHECK(cudaEventCreate(&e0));
-    CCDK_CUDA_CHECK(cudaEventCreate(&e1));
+    cudaEvent_t e0 = c.events.get(EventPool::kNarrow), e1 = c.events.get(EventPool::kNarrow + 1);
     CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
     if (n > 0 && n > in.queue_capacity) {
         // narrowphase.cpp:215-218: seeds alone exceed the capacity
@@ -832,8 +839,6 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     float ms = 0;
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
     st.device_ms = ms;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     if (st.overflow) {
         st.global_toi = INFINITY;
     }

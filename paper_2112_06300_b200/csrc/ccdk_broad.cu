@@ -502,8 +502,8 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         throw Error(CCDK_CONFIG, "broad phase: more than 2^32-2 boxes");
 
     cudaEvent_t ev[4];
-    for (auto& e : ev)
-        CCDK_CUDA_CHECK(cudaEventCreate(&e));
+    for (int i = 0; i < 4; ++i)
+        ev[i] = c.events.get(EventPool::kBroad + i);
     CCDK_CUDA_CHECK(cudaEventRecord(ev[0], s));
 
     auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
@@ -691,8 +691,6 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_axis_sort, ev[0], ev[1]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_sweep, ev[1], ev[2]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_pairsort, ev[2], ev[3]));
-    for (auto& e : ev)
-        cudaEventDestroy(e);
     out.axis = axis;
     out.n_pairs = n_pairs;
     c.last_n_pairs = n_pairs;

@@ -138,6 +138,32 @@ struct PinnedBuf {
     }
 };
 
+// Timing events, created once per context (creating/destroying events per
+// call takes driver locks; fixed slots per call site, each slot's use is
+// synchronised before its next record).
+struct EventPool {
+    enum { kStep = 0, kBatch = 6, kBroad = 8, kNarrow = 12, kApi = 16, kSlots = 20 };
+    cudaEvent_t ev[kSlots] = {};
+    EventPool() = default;
+    EventPool(const EventPool&) = delete;
+    EventPool& operator=(const EventPool&) = delete;
+    ~EventPool()
+    {
+        for (auto e : ev)
+            if (e)
+                cudaEventDestroy(e);
+    }
+    cudaEvent_t get(int i)
+    {
+        if (!ev[i]) {
+            const cudaError_t r = cudaEventCreate(&ev[i]);
+            if (r != cudaSuccess)
+                throw Error(CCDK_CUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(r));
+        }
+        return ev[i];
+    }
+};
+
 // Device-side scene (canonical slot order V, E, F; aabb.cpp:79-105).
 struct DevScene {
     DevBuf v0, v1, edges, faces;
@@ -309,6 +335,9 @@ struct Ctx {
     DevBuf nscal;                      // NarrowScalars
     GenGraph gen_graph;
     int gen_blocks_per_sm = 0;
+    uint64_t mem_probe_n = 0;          // narrow interval capacity probed for this many queries
+    uint64_t mem_probe_cap = 0;
+    EventPool events;
     uint64_t last_query_count = 0;
     uint64_t narrow_launches = 0;
     uint64_t narrow_any_flags = 0;

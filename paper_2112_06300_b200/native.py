@@ -58,6 +58,9 @@ _SIGS = {
     "ccdk_fetch_round_sizes": (C.c_int, [C.c_void_p, P_U64]),
     "ccdk_classify": (C.c_int, [C.c_void_p, P_U64, C.c_uint64, P_F64, P_F64, C.c_uint64, P_U32,
                                 C.c_uint64, P_U32, C.c_uint64, P_U8, P_F64, P_U64, P_U64, P_U64]),
+    "ccdk_narrow_phase_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                           C.POINTER(abi.NarrowCfg), C.c_uint64, C.c_void_p, C.c_void_p,
+                                           C.POINTER(abi.NarrowStats)]),
     "ccdk_inclusion_boxes": (C.c_int, [C.c_void_p, P_U8, P_F64, P_F64, C.c_uint64, P_F64]),
     "ccdk_process_intervals": (C.c_int, [C.c_void_p, P_U8, P_F64, P_F64, P_U16, P_F64, P_F64,
                                          C.c_uint64, C.POINTER(abi.NarrowCfg), P_U8, P_F64, P_U8,

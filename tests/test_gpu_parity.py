@@ -429,3 +429,37 @@ def test_query_results_fetch(ctx, ref):
     etoi, eflags, _ = ref.narrow_phase(cls[0], cls[1], NarrowConfig().to_c())
     assert_bits(toi, etoi)
     np.testing.assert_array_equal(flags, eflags)
+
+
+# ------------------------------------------------------- C5 (narrow-only batch)
+
+def test_c5_mixed_sample_bit_exact(ctx, ref):
+    """BASELINE config 5 recipe on a sample: generic queries with every
+    1,000th replaced by a rotated near-degenerate (plane crossings, tangent
+    double roots, parallel-above, coincident, slides) plus two slides at gap
+    2e-6 that exhaust the 2^20 split budget (the config's work bombs)."""
+    import os
+    import oracle
+    qb = concat(scenes.mixed_queries(20_000, seed=1003, every=1000, n_exhaust=0),
+                scenes.degenerate_queries(2, seed=77, n_exhaust=2))
+    got = ck.narrow_phase(qb, ctx=ctx)
+    toi, flags, st = oracle.ref(os.cpu_count() or 1).narrow_phase(qb.kind, qb.points, NarrowConfig().to_c())
+    _narrow_equal(got, toi, flags, st)
+    assert (got.flags[-2:] & abi.FLAG_TOLERANCE_HIT).any()  # the VF budget bomb really exhausts
+
+
+def test_c5_partition_independence(ctx):
+    """Size-independent property at C5 scale: a query's result depends only
+    on the query (narrowphase.hpp:93-96), so per-query ToI/flags of a 2M-query
+    batch equal those of the same queries run as a small separate batch, and
+    the global ToI is the min of the per-query ToIs."""
+    qb = scenes.mixed_queries(2_000_000, seed=1003, every=10000, n_exhaust=4)
+    big = ck.narrow_phase(qb, ctx=ctx)
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([rng.choice(len(qb), 4000, replace=False),
+                                    np.arange(9999, len(qb), 10000)]))
+    small = ck.narrow_phase(scenes.QueryBatch(qb.kind[idx], qb.points[idx]), ctx=ctx)
+    assert_bits(big.toi[idx], small.toi)
+    np.testing.assert_array_equal(big.flags[idx], small.flags)
+    assert big.global_toi == big.toi.min()
+    assert int((big.flags & abi.FLAG_TOLERANCE_HIT).astype(bool).sum()) >= 1  # a budget bomb is in the batch
