@@ -419,33 +419,136 @@ __global__ void __launch_bounds__(kTB) k_sweep_tile(SweepArgs a)
     }
 }
 
-// Heavy rows: one warp per (row, SEG-long window segment), coalesced loads.
-__global__ void __launch_bounds__(256) k_sweep_heavy(SweepArgs a)
+// K5 sweep, row-parallel form: one warp per row at a time, lanes over the
+// row's window [p+1, min(run_end, p+1+kCap)) in 32-box strides with
+// coalesced float4 loads.  A warp walks kRowsPerWarp consecutive rows and a
+// CTA 8 warps of them, so neighbouring windows (which overlap almost
+// entirely) are served from L1; no block barrier, and a lane tests only boxes
+// of its own row's window (the ragged tail costs < 32 lanes per row).
+// Three-axis overlaps (~3% of tests on cloth, so most 32-box strides hold
+// one) are compacted into a per-warp list and the adjacency/kind filter
+// (keep_pair, which needs the other box's vertex ids) runs on 32 of them at a
+// time with every lane busy, instead of a dependent load per stride.  Rows
+// whose window exceeds kCap spill the rest to k_sweep_heavy segments.
+constexpr int kRowsPerWarp = 8;
+constexpr int kRowsTB = 256;
+#ifndef CCDK_SWEEP_UNROLL
+#define CCDK_SWEEP_UNROLL 4
+#endif
+constexpr int kUnroll = CCDK_SWEEP_UNROLL;
+constexpr int kHitBuf = 32 * kUnroll + 32; // < 32 left over + kUnroll strides
+
+__device__ __forceinline__ void filter_hits(const SweepArgs& a, unsigned long long p, uint4 mv,
+                                            const unsigned* hits, unsigned cnt, unsigned lane)
 {
-    const unsigned long long nseg = *a.n_heavy;
+    const bool h = lane < cnt;
+    const unsigned long long q = p + (h ? hits[lane] : 0u);
+    const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
+    emit(a, h && keep_pair(mv, ov) && bf_ok(a, p, q), mv.w, ov.w);
+}
+
+// Run the filter on every full chunk of 32 (all of them when `all`) and
+// move the remainder to the front of the list.
+__device__ __forceinline__ void drain_hits(const SweepArgs& a, unsigned long long p, uint4 mv,
+                                           unsigned* hits, unsigned& nh, unsigned lane, bool all)
+{
+    __syncwarp();
+    unsigned base = 0;
+    while (nh - base >= 32 || (all && nh > base)) {
+        const unsigned cnt = min(nh - base, 32u);
+        filter_hits(a, p, mv, hits + base, cnt, lane);
+        base += cnt;
+    }
+    const unsigned rem = nh - base; // < 32
+    const unsigned v = lane < rem ? hits[base + lane] : 0u;
+    __syncwarp();
+    if (lane < rem)
+        hits[lane] = v;
+    __syncwarp();
+    nh = rem;
+}
+
+__device__ __forceinline__ void push_hit(unsigned* hits, unsigned& nh, bool h, unsigned off, unsigned lane)
+{
+    const unsigned m = __ballot_sync(0xffffffffu, h);
+    if (h)
+        hits[nh + __popc(m & ((1u << lane) - 1))] = off;
+    nh += __popc(m);
+}
+
+// Row p against boxes [jb, je) of its window (warp-cooperative).
+__device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long long p, unsigned long long jb,
+                                             unsigned long long je, unsigned* hits, unsigned lane)
+{
+    const float4 mb = a.sbox[p];
+    const uint4 mv = a.svid[p];
+    unsigned nh = 0;             // warp-uniform
+    unsigned long long j0 = jb;  // warp-uniform stride base
+    // kUnroll full strides per iteration: all loads in flight before the tests
+    for (; j0 + 32 * kUnroll <= je; j0 += 32 * kUnroll) {
+        const unsigned long long j = j0 + lane;
+        float4 o[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            o[u] = __ldg(&a.sbox[j + 32 * u]);
+        bool h[kUnroll], any = false;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            h[u] = box_hit(mb, o[u]);
+            any = any || h[u];
+        }
+        if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                push_hit(hits, nh, h[u], static_cast<unsigned>(j + 32 * u - p), lane);
+            if (nh >= 32)
+                drain_hits(a, p, mv, hits, nh, lane, false);
+        }
+    }
+    // ragged tail (< 32 kUnroll boxes): lanes past the window end are idle
+    for (; j0 < je; j0 += 32) {
+        const unsigned long long j = j0 + lane;
+        const bool valid = j < je;
+        const bool h = valid && box_hit(mb, __ldg(&a.sbox[valid ? j : p]));
+        push_hit(hits, nh, h, static_cast<unsigned>(j - p), lane);
+    }
+    if (nh)
+        drain_hits(a, p, mv, hits, nh, lane, true);
+}
+
+__global__ void __launch_bounds__(kRowsTB) k_sweep_rows(SweepArgs a)
+{
+    __shared__ unsigned s_hits[kRowsTB / 32][kHitBuf];
     const unsigned lane = threadIdx.x & 31;
+    unsigned* hits = s_hits[threadIdx.x >> 5];
+    const unsigned long long B = a.range[0], E = a.range[1];
+    const unsigned long long warp = (blockIdx.x * static_cast<unsigned long long>(kRowsTB) + threadIdx.x) >> 5;
+    const unsigned long long p0 = a.row0 + warp * kRowsPerWarp;
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+        const unsigned long long p = p0 + r;
+        if (p >= E)
+            break; // warp-uniform
+        if (p < B)
+            continue;
+        const unsigned long long je = min(static_cast<unsigned long long>(a.run_end[p]), p + 1 + kCap);
+        if (je > p + 1)
+            sweep_window(a, p, p + 1, je, hits, lane);
+    }
+}
+
+// Heavy rows: one warp per (row, kSeg-long window segment) — the part of a
+// window beyond kCap (static floors / container walls whose window is ~k).
+__global__ void __launch_bounds__(kRowsTB) k_sweep_heavy(SweepArgs a)
+{
+    __shared__ unsigned s_hits[kRowsTB / 32][kHitBuf];
+    const unsigned lane = threadIdx.x & 31;
+    unsigned* hits = s_hits[threadIdx.x >> 5];
+    const unsigned long long nseg = *a.n_heavy;
     const unsigned long long warp = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5;
     const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
-    for (unsigned long long s = warp; s < nseg; s += nwarps) {
-        const Seg g = a.segs[s];
-        const float4 mb = a.sbox[g.p];
-        const uint4 mv = a.svid[g.p];
-        for (uint32_t j0 = g.jb; j0 < g.je; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            bool hit = false;
-            float4 o;
-            if (j < g.je) {
-                o = a.sbox[j];
-                hit = box_hit(mb, o);
-            }
-            if (__any_sync(0xffffffffu, hit)) {
-                uint4 ov = make_uint4(0, 0, 0, 0);
-                if (hit)
-                    ov = a.svid[j];
-                const bool keep = hit && keep_pair(mv, ov) && bf_ok(a, g.p, j);
-                emit(a, keep, mv.w, ov.w);
-            }
-        }
+    for (unsigned long long sg = warp; sg < nseg; sg += nwarps) {
+        const Seg g = a.segs[sg];
+        sweep_window(a, g.p, g.jb, g.je, hits, lane);
     }
 }
 
@@ -652,9 +755,16 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         sa.n_pairs = &ctr->n_pairs;
         sa.segs = segs;
         sa.n_heavy = &ctr->n_heavy;
+#ifndef CCDK_SWEEP_TILE
+        if (hi > lo) {
+            const uint64_t warps = (hi - lo + kRowsPerWarp - 1) / kRowsPerWarp;
+            k_sweep_rows<<<grid_for(warps * 32, kRowsTB), kRowsTB, 0, s>>>(sa);
+        }
+#else
         if (hi > lo)
             k_sweep_tile<<<grid_for(hi - lo, kTB), kTB, 0, s>>>(sa);
-        k_sweep_heavy<<<4 * c.num_sms, 256, 0, s>>>(sa);
+#endif
+        k_sweep_heavy<<<4 * c.num_sms, kRowsTB, 0, s>>>(sa);
         CCDK_LAUNCH_CHECK();
         read_ctr();
         n_pairs = host_ctr[0];
