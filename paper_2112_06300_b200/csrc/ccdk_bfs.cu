@@ -32,8 +32,22 @@ constexpr unsigned kNoGen = 0xffffffffu;
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr int kGenBlock = 128;
 #ifndef CCDK_GEN_MINB
-#define CCDK_GEN_MINB 4
+#define CCDK_GEN_MINB 3
 #endif
+
+// Interval storage.  Every split appends ONE record — the split interval
+// itself (query id, (t,u,v).lo, packed depths) — to the region of its split
+// dimension; the record stands for its two children (lower and upper half
+// along that dimension, narrowphase.cpp:122-132), which the next generation
+// evaluates together (iv::process_pair).  Generation 0 evaluates the roots
+// [0,1]^3 (one per query, implicit).
+struct Region {
+    uint32_t* qid;
+    double* t;
+    double* u;
+    double* v;
+    unsigned long long* dep;
+};
 
 struct GenArgs {
     uint32_t* qf;      // per-query kind | exact-widening flag (iv::kKind*)
@@ -51,16 +65,11 @@ struct GenArgs {
     unsigned* dirty;                 // queries whose ToI dropped (duplicates allowed)
     unsigned long long dirty_cap;    // beyond it k_finish refreshes every query
     unsigned long long nq;           // queries in this run
-    uint32_t* qid[2];
-    double* t[2];
-    double* u[2];
-    double* v[2];
-    unsigned long long* dep[2];
-    unsigned long long phys_cap;
+    Region reg[2][3];                // [generation parity][split dimension]
+    unsigned long long cap_pairs;    // records per region buffer
     unsigned long long sem_cap;
     NarrowScalars* sc;
     cudaGraphConditionalHandle cond; // WHILE node of the generation graph
-    unsigned zero;                   // always 0 (see atom_add_u64)
 };
 
 __device__ __forceinline__ unsigned long long dbits(double x)
@@ -80,268 +89,355 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// Per-warp smem stages, element-major (element e of lane l at [32 e + l]) so
-// a warp reading element e touches 32 consecutive doubles:
-//   coordinates: 24 doubles per lane, double-buffered (batch b is evaluated
-//                from one buffer while batch b+W streams into the other);
-//   metadata:    the interval record (t, u, v lo, depths) and the per-query
-//                scalars (snapshot ToI, separation, exhausted generation |
-//                query flags), single-buffered: it is read into registers
-//                before the next batch's copy is issued.
-// Everything a batch needs arrives by cp.async, so no register load is in
-// flight across the evaluation (a register prefetch ties up scoreboards and
-// was measured to stall the loop head on the L2 round trip).
-constexpr int kStageDoubles = 24 * 32;
-constexpr int kMetaDoubles = 7 * 32;
-constexpr int kQidDoubles = 16; // 32 query ids (u32) of batch b+W
-#ifndef CCDK_GEN_STAGES
-#define CCDK_GEN_STAGES 1 // coordinate buffers per warp (1: the copy of batch b+W waits for b's evaluation)
-#endif
-constexpr int kStages = CCDK_GEN_STAGES;
-constexpr int kWarpSmemDoubles = kStages * kStageDoubles + kMetaDoubles + kQidDoubles;
-constexpr int kGenSmem = (kGenBlock / 32) * kWarpSmemDoubles * sizeof(double);
-enum { kMT = 0, kMU, kMV, kMDep, kMSnap, kMSep, kMExh };
-
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Issue batch bb's copies: lane's interval i (if valid) of query q.
-__device__ __forceinline__ void stage_batch(const GenArgs& a, int cb, double* coords, double* meta,
-                                            unsigned lane, unsigned long long i, unsigned q)
+// Collision of one interval: fold its t.lo into the query's live ToI and
+// queue the query for the snapshot refresh (cand = t.lo < the snapshot, else
+// the box would have been pruned, so the ToI drops this generation).
+__device__ __forceinline__ void record_collision(const GenArgs& a, unsigned q, double cand, bool zd)
 {
-    const double* src = a.pts + 24ull * q;
-#pragma unroll
-    for (int e = 0; e < 24; ++e)
-        cp_async8(coords + 32 * e + lane, src + e);
-    cp_async8(meta + 32 * kMT + lane, a.t[cb] + i);
-    cp_async8(meta + 32 * kMU + lane, a.u[cb] + i);
-    cp_async8(meta + 32 * kMV + lane, a.v[cb] + i);
-    cp_async8(meta + 32 * kMDep + lane, a.dep[cb] + i);
-    cp_async8(meta + 32 * kMSnap + lane, a.snap + q);
-    if (a.sep)
-        cp_async8(meta + 32 * kMSep + lane, a.sep + q);
-    unsigned* ex = reinterpret_cast<unsigned*>(meta + 32 * kMExh + lane);
-    cp_async4(ex, a.exh_gen + q);
-    cp_async4(ex + 1, a.qf + q);
+    atomicMin(&a.toi[q], dbits(cand));
+    const unsigned long long slot = atomicAdd(&a.sc->dirty_n, 1ull);
+    if (slot < a.dirty_cap)
+        a.dirty[slot] = q;
+    if (zd)
+        a.zdiag[q] = 1;
 }
 
-// Plain atomic add with the old value returned, on an address the compiler
-// cannot prove warp-uniform (callers offset it by `zero * lane`, zero a
-// runtime 0): ptxas rewrites uniform-address atomics into a warp-aggregated
-// form that broadcasts the result with a shuffle right after the atomic, i.e.
-// it would wait for the round trip that this kernel defers by a whole batch.
-__device__ __forceinline__ unsigned long long atom_add_u64(unsigned long long* p, unsigned long long v)
-{
-    unsigned long long old;
-    asm volatile("atom.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
-    return old;
-}
-
-// Children of an admitted split, written one batch after the split so the
-// append-cursor and split-budget atomics overlap the next evaluation.
-struct Pending {
-    unsigned long long slot_raw;   // leader's atomicAdd result (all lanes after shfl)
-    unsigned long long split_old;  // this lane's split-request counter before the request
-    unsigned long long dp;
+// Split records of this batch: per lane up to two (one per child), each
+// appended to the region of its split dimension with one warp-aggregated
+// cursor atomic per region.
+struct SplitRec {
+    int dim; // -1: none
     double tlo, ulo, vlo;
-    unsigned long long dirty_slot; // dirty-list slot of a collision
-    unsigned q;
-    unsigned mask;                 // admit ballot of the batch
-    int dim;
-    int leader;
-    bool counted;                  // split_old holds a real request
-    bool collided;                 // this lane recorded a collision
+    unsigned long long dp;
 };
 
-__device__ __forceinline__ void finish_pending(const GenArgs& a, int nb, unsigned lane, unsigned gen,
-                                               const Pending& p)
+__device__ __forceinline__ void append_splits(const GenArgs& a, int nb, unsigned lane, unsigned q,
+                                              const SplitRec r[2])
 {
-    if (p.collided && p.dirty_slot < a.dirty_cap)
-        a.dirty[p.dirty_slot] = p.q;
-    if (!p.mask)
-        return;
-    const unsigned long long slot0 = __shfl_sync(0xffffffffu, p.slot_raw, p.leader);
-    if (p.mask & (1u << lane)) {
-        const unsigned long long s = slot0 + 2ull * __popc(p.mask & ((1u << lane) - 1));
-        if (s + 2 <= a.phys_cap) {
-            const unsigned dd = (p.dp >> (16 * p.dim)) & 0xffff;
-            const double lo = p.dim == 0 ? p.tlo : p.dim == 1 ? p.ulo : p.vlo;
-            // split_box (narrowphase.cpp:122-132): exact midpoint of a dyadic interval
-            const double mid = __dadd_rn(lo, __dmul_rn(0.5, iv::dyadic_width(dd)));
-            const unsigned long long dpc = p.dp + (1ull << (16 * p.dim));
-            a.qid[nb][s] = p.q;
-            a.qid[nb][s + 1] = p.q;
-            a.t[nb][s] = p.tlo;
-            a.t[nb][s + 1] = p.dim == 0 ? mid : p.tlo;
-            a.u[nb][s] = p.ulo;
-            a.u[nb][s + 1] = p.dim == 1 ? mid : p.ulo;
-            a.v[nb][s] = p.vlo;
-            a.v[nb][s + 1] = p.dim == 2 ? mid : p.vlo;
-            a.dep[nb][s] = dpc;
-            a.dep[nb][s + 1] = dpc;
-        } else {
-            a.sc->phys_overflow = 1;
+    const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const unsigned m0 = __ballot_sync(0xffffffffu, r[0].dim == d);
+        const unsigned m1 = __ballot_sync(0xffffffffu, r[1].dim == d);
+        const unsigned cnt = __popc(m0) + __popc(m1);
+        if (!cnt)
+            continue;
+        const int leader = __ffs(m0 | m1) - 1;
+        unsigned long long base = 0;
+        if (lane == static_cast<unsigned>(leader))
+            base = atomicAdd(&a.sc->next_pairs[d], static_cast<unsigned long long>(cnt));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        const Region& R = a.reg[nb][d];
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+            if (r[ch].dim != d)
+                continue;
+            const unsigned long long slot = base + (ch ? __popc(m0) + __popc(m1 & lt) : __popc(m0 & lt));
+            if (slot < a.cap_pairs) {
+                R.qid[slot] = q;
+                R.t[slot] = r[ch].tlo;
+                R.u[slot] = r[ch].ulo;
+                R.v[slot] = r[ch].vlo;
+                R.dep[slot] = r[ch].dp;
+            } else {
+                a.sc->phys_overflow = 1;
+            }
         }
-        if (p.counted && p.split_old >= a.max_splits)
-            a.exh_gen[p.q] = gen; // budget exhausted (narrowphase.cpp:263-271)
     }
 }
 
-// One BFS generation: process_interval on every live interval + the fold
-// (narrowphase.cpp:226-305).  Each warp walks batches of 32 intervals
-// (stride W = number of warps) with a two-deep software pipeline: batch b is
-// evaluated from shared memory while batch b+W's coordinates and metadata
-// stream in by cp.async and batch b+2W's query ids load into a register; the
-// children of batch b are appended after batch b+W's evaluation (their
-// cursor atomic is issued at the end of batch b).
+// ---- generation 0: the roots [0,1]^3, one thread per query, coordinates
+// read straight from the query record (one generation of the ~80).
+__global__ void __launch_bounds__(kGenBlock) k_gen0(GenArgs a)
+{
+    NarrowScalars* sc = a.sc;
+    const unsigned lane = threadIdx.x & 31;
+    unsigned evals = 0, split_actions = 0;
+    const unsigned long long n = a.nq;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    // warp-uniform trip count (the append is warp-collective)
+    const unsigned long long n_up = (n + 31) & ~31ull;
+    for (unsigned long long q0 = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         q0 < n_up; q0 += stride) {
+        const bool valid = q0 < n;
+        const unsigned q = static_cast<unsigned>(valid ? q0 : 0);
+        SplitRec r[2];
+        r[0].dim = r[1].dim = -1;
+        if (valid) {
+            const iv::Box bx { 0.0, 1.0, 0.0, 1.0, 0.0, 1.0 };
+            const unsigned qf = a.qf[q];
+            const bool vf = !(qf & iv::kKindEE);
+            const double sep = a.sep ? a.sep[q] : a.sep_default;
+            const iv::GlobalPts P { a.pts + 24ull * q };
+            double cand = 0;
+            bool zd = false, evald = false;
+            int dim = -1, act;
+            if (!(qf & iv::kKindExact)) {
+                act = iv::process_one<iv::Fast>(vf, P, bx, CUDART_INF, sep, a.cfg, cand, zd, dim, evald);
+            } else {
+                const iv::Outcome o = iv::process_exact<iv::GlobalPts>(vf, P, bx, CUDART_INF, sep, a.cfg);
+                act = o.act;
+                cand = o.cand;
+                zd = o.zdiag;
+                dim = o.dim;
+                evald = o.evaluated;
+            }
+            evals += evald;
+            if (act == iv::kCollision) {
+                record_collision(a, q, cand, zd);
+            } else if (act == iv::kSplit) {
+                ++split_actions;
+                // t.lo == 0 here: exempt from the budget in no-zero-ToI mode
+                if (!a.cfg.no_zero_toi) {
+                    const unsigned long long old = atomicAdd(&a.splits[q], 1ull);
+                    if (old >= a.max_splits)
+                        a.exh_gen[q] = 0;
+                }
+                r[0] = { dim, 0.0, 0.0, 0.0, 0ull };
+            }
+        }
+        append_splits(a, 1, lane, q, r);
+    }
+    warp_add(&sc->evaluations, evals);
+    warp_add(&sc->split_actions, split_actions);
+}
+
+// ---- generations >= 1: one lane per split record (= a sibling pair).
+//
+// Per-warp shared-memory stage, element-major (element e of lane l at
+// [32 e + l]): the query coordinates (24 doubles), the record (t, u, v lo,
+// depths), and the per-query scalars (snapshot ToI, separation, exhausted
+// generation | query flags), all brought in by cp.async while the previous
+// batch is evaluated; the next batch's query ids ride one batch ahead.
+constexpr int kStageDoubles = 24 * 32;
+constexpr int kMetaDoubles = 7 * 32;
+constexpr int kQidDoubles = 16;
+constexpr int kWarpSmemDoubles = 2 * kStageDoubles + kMetaDoubles + kQidDoubles;
+constexpr int kGenSmem = (kGenBlock / 32) * kWarpSmemDoubles * sizeof(double);
+enum { kMT = 0, kMU, kMV, kMDep, kMSnap, kMSep, kMExh };
+
+struct BatchLoc {
+    int d;                    // region (split dimension)
+    unsigned long long i0;    // first record of the batch
+    unsigned long long n;     // records in the region
+};
+
+__device__ __forceinline__ BatchLoc locate(const unsigned long long nbr[3], const unsigned long long cnt[3],
+                                           unsigned long long b)
+{
+    BatchLoc L;
+    if (b < nbr[0]) {
+        L.d = 0;
+    } else if (b < nbr[0] + nbr[1]) {
+        L.d = 1;
+        b -= nbr[0];
+    } else {
+        L.d = 2;
+        b -= nbr[0] + nbr[1];
+    }
+    L.i0 = b << 5;
+    L.n = cnt[L.d];
+    return L;
+}
+
+template <int D>
+__device__ __forceinline__ iv::PairOutcome eval_pair(bool vf, const iv::SmemPts& P, const iv::PairBox& pb,
+                                                     const bool alive[2], double sep, const iv::Cfg& cfg)
+{
+    return iv::process_pair<D, iv::SmemPts>(vf, P, pb, alive, sep, cfg);
+}
+
 __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs a)
 {
     extern __shared__ double gsm[];
     NarrowScalars* sc = a.sc;
     if (!sc->cont)
         return;
-    const unsigned long long n = sc->cur_n;
     const unsigned gen = static_cast<unsigned>(sc->gen);
     const int cb = gen & 1, nb = cb ^ 1;
-    const uint32_t* __restrict__ qid = a.qid[cb];
+    unsigned long long cnt[3], nbr[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        cnt[d] = sc->cur_pairs[d];
+        nbr[d] = (cnt[d] + 31) >> 5;
+    }
+    const unsigned long long nbatch = nbr[0] + nbr[1] + nbr[2];
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
-    double* coords = gsm + wib * kWarpSmemDoubles;
-    double* meta = coords + kStages * kStageDoubles;
-    const unsigned long long nbatch = (n + 31) >> 5;
+    double* stage0 = gsm + wib * kWarpSmemDoubles;
+    double* meta = stage0 + 2 * kStageDoubles;
+    unsigned* qbuf = reinterpret_cast<unsigned*>(meta + kMetaDoubles);
     const unsigned long long W = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long b = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x >> 5) + wib;
     unsigned evals = 0, split_actions = 0, dropped = 0;
     if (b >= nbatch)
         return; // warp-uniform; no __syncthreads in this kernel
 
-    unsigned* qbuf = reinterpret_cast<unsigned*>(meta + kMetaDoubles);
-    auto in_range = [&](unsigned long long bb) { return bb < nbatch && (bb << 5) + lane < n; };
     auto issue = [&](unsigned long long bb, unsigned q, int st) {
-        // batch bb's data (its query ids are known) and batch bb+W's query ids
-        if (in_range(bb))
-            stage_batch(a, cb, coords + st * kStageDoubles, meta, lane, (bb << 5) + lane, q);
-        if (in_range(bb + W))
-            cp_async4(qbuf + lane, qid + ((bb + W) << 5) + lane);
+        // batch bb's coordinates + record + query scalars, batch bb+W's ids
+        if (bb < nbatch) {
+            const BatchLoc L = locate(nbr, cnt, bb);
+            const unsigned long long i = L.i0 + lane;
+            if (i < L.n) {
+                const Region& R = a.reg[cb][L.d];
+                double* coords = stage0 + st * kStageDoubles;
+                const double* src = a.pts + 24ull * q;
+#pragma unroll
+                for (int e = 0; e < 24; ++e)
+                    cp_async8(coords + 32 * e + lane, src + e);
+                cp_async8(meta + 32 * kMT + lane, R.t + i);
+                cp_async8(meta + 32 * kMU + lane, R.u + i);
+                cp_async8(meta + 32 * kMV + lane, R.v + i);
+                cp_async8(meta + 32 * kMDep + lane, R.dep + i);
+                cp_async8(meta + 32 * kMSnap + lane, a.snap + q);
+                if (a.sep)
+                    cp_async8(meta + 32 * kMSep + lane, a.sep + q);
+                unsigned* ex = reinterpret_cast<unsigned*>(meta + 32 * kMExh + lane);
+                cp_async4(ex, a.exh_gen + q);
+                cp_async4(ex + 1, a.qf + q);
+            }
+        }
+        if (bb + W < nbatch) {
+            const BatchLoc L = locate(nbr, cnt, bb + W);
+            const unsigned long long i = L.i0 + lane;
+            if (i < L.n)
+                cp_async4(qbuf + lane, a.reg[cb][L.d].qid + i);
+        }
         cp_async_commit();
     };
 
-    unsigned q_cur = in_range(b) ? qid[(b << 5) + lane] : 0u;
+    unsigned q_cur;
+    {
+        const BatchLoc L = locate(nbr, cnt, b);
+        const unsigned long long i = L.i0 + lane;
+        q_cur = i < L.n ? a.reg[cb][L.d].qid[i] : 0u;
+    }
     issue(b, q_cur, 0);
     int st = 0;
-    Pending pend {}; // nothing pending before the first batch (mask 0, no collision)
 
     for (; b < nbatch; b += W) {
-        cp_async_wait<0>(); // batch b's coordinates + metadata, batch b+W's ids (issued one batch ago)
-        const unsigned long long i = (b << 5) + lane;
-        const bool valid = i < n;
+        cp_async_wait<0>(); // batch b's data and batch b+W's ids (issued one batch ago)
+        const BatchLoc L = locate(nbr, cnt, b);
+        const bool valid = L.i0 + lane < L.n;
         const unsigned q = q_cur;
         const double tlo = meta[32 * kMT + lane];
         const double ulo = meta[32 * kMU + lane];
         const double vlo = meta[32 * kMV + lane];
         const unsigned long long dp = static_cast<unsigned long long>(__double_as_longlong(meta[32 * kMDep + lane]));
-        const unsigned long long snap = static_cast<unsigned long long>(__double_as_longlong(meta[32 * kMSnap + lane]));
+        const double t_star = meta[32 * kMSnap + lane];
         const double sep = a.sep ? meta[32 * kMSep + lane] : a.sep_default;
         const unsigned exh = reinterpret_cast<const unsigned*>(meta + 32 * kMExh + lane)[0];
         const unsigned qf = reinterpret_cast<const unsigned*>(meta + 32 * kMExh + lane)[1];
         q_cur = qbuf[lane];
-        // batch b+W: copies into the other coordinate buffer and the (now
-        // consumed) metadata stage; batch b+2W: query ids
-        if (kStages == 2)
-            issue(b + W, q_cur, st ^ 1);
+        // batch b+W streams into the other coordinate buffer while b is evaluated
+        issue(b + W, q_cur, st ^ 1);
 
-        bool admit = false, collided = false;
-        int dim = -1;
+        SplitRec r[2];
+        r[0].dim = r[1].dim = -1;
         if (valid) {
+            const int D = L.d;
             if (exh < gen) {
-                // exhausted in an earlier generation: fold t.lo and drop
+                // exhausted in an earlier generation: fold the children's
+                // min t.lo (= the record's t.lo) and drop both
                 // (narrowphase.cpp:280-291)
                 atomicMin(&a.toi[q], dbits(tlo));
                 if (a.cfg.no_zero_toi && tlo == 0.0)
                     a.zdiag[q] = 1;
-                ++dropped;
+                dropped += 2;
             } else {
-                iv::Box bx;
-                bx.tlo = tlo;
-                bx.thi = __dadd_rn(tlo, iv::dyadic_width(dp & 0xffff));
-                bx.ulo = ulo;
-                bx.uhi = __dadd_rn(ulo, iv::dyadic_width((dp >> 16) & 0xffff));
-                bx.vlo = vlo;
-                bx.vhi = __dadd_rn(vlo, iv::dyadic_width((dp >> 32) & 0xffff));
-                const double t_star = __longlong_as_double(static_cast<long long>(snap));
+                // the pair's samples: (lo, mid, hi) along D, (lo, hi) elsewhere
+                const unsigned dD = (dp >> (16 * D)) & 0xffff;
+                iv::PairBox pb;
+                const double wt = iv::dyadic_width(dp & 0xffff);
+                const double wu = iv::dyadic_width((dp >> 16) & 0xffff);
+                const double wv = iv::dyadic_width((dp >> 32) & 0xffff);
+                pb.t[0] = tlo;
+                pb.u[0] = ulo;
+                pb.v[0] = vlo;
+                // split_box (narrowphase.cpp:122-132): the exact dyadic midpoint
+                const double mid = __dadd_rn(D == 0 ? tlo : D == 1 ? ulo : vlo, iv::dyadic_width(dD + 1));
+                pb.t[1] = D == 0 ? mid : __dadd_rn(tlo, wt);
+                pb.t[2] = __dadd_rn(tlo, wt);
+                pb.u[1] = D == 1 ? mid : __dadd_rn(ulo, wu);
+                pb.u[2] = __dadd_rn(ulo, wu);
+                pb.v[1] = D == 2 ? mid : __dadd_rn(vlo, wv);
+                pb.v[2] = __dadd_rn(vlo, wv);
                 const bool vf = !(qf & iv::kKindEE);
-                const iv::SmemPts P { coords + st * kStageDoubles + lane };
-                double cand = 0;
-                bool zd = false, evald = false;
-                int act;
-                if (!(qf & iv::kKindExact))
-                    act = iv::process_one<iv::Fast>(vf, P, bx, t_star, sep, a.cfg, cand, zd, dim, evald);
-                else {
-                    const iv::Outcome o = iv::process_exact<iv::SmemPts>(vf, P, bx, t_star, sep, a.cfg);
-                    act = o.act;
-                    cand = o.cand;
-                    zd = o.zdiag;
-                    dim = o.dim;
-                    evald = o.evaluated;
+                bool alive[2];
+                double clo[2][3];
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {
+                    clo[ch][0] = (D == 0 && ch) ? mid : tlo;
+                    clo[ch][1] = (D == 1 && ch) ? mid : ulo;
+                    clo[ch][2] = (D == 2 && ch) ? mid : vlo;
+                    // process_interval's pre-evaluation prunes (narrowphase.cpp:138-143)
+                    alive[ch] = !(clo[ch][0] >= t_star || clo[ch][0] >= a.cfg.t_max)
+                        && !(vf && __dadd_rn(clo[ch][1], clo[ch][2]) > 1.0);
                 }
-                evals += evald;
-                if (act == iv::kCollision) {
-                    // cand = t.lo < the snapshot (else the box was pruned), so
-                    // the query's ToI drops this generation: queue it for the
-                    // snapshot refresh (slot written one batch later)
-                    atomicMin(&a.toi[q], dbits(cand));
-                    collided = true;
-                    if (zd)
-                        a.zdiag[q] = 1;
-                } else if (act == iv::kSplit) {
-                    // Every split is appended; a request beyond the budget
-                    // marks the query exhausted in this generation; its
-                    // children are then folded (min t.lo, zdiag at t.lo == 0)
-                    // and dropped at the start of the next one, which equals
-                    // the reference's fold of every split interval of the
-                    // exhausting generation (narrowphase.cpp:254-297): a
-                    // child's t.lo is >= its parent's and the left child's
-                    // equals it.
-                    ++split_actions;
-                    admit = true;
+                if (alive[0] || alive[1]) {
+                    const iv::SmemPts P { stage0 + st * kStageDoubles + lane };
+                    iv::PairOutcome o;
+                    if (!(qf & iv::kKindExact)) {
+                        if (D == 0)
+                            o = eval_pair<0>(vf, P, pb, alive, sep, a.cfg);
+                        else if (D == 1)
+                            o = eval_pair<1>(vf, P, pb, alive, sep, a.cfg);
+                        else
+                            o = eval_pair<2>(vf, P, pb, alive, sep, a.cfg);
+                    } else {
+#pragma unroll
+                        for (int ch = 0; ch < 2; ++ch) {
+                            o.act[ch] = iv::kPruned;
+                            o.evaluated[ch] = false;
+                            if (!alive[ch])
+                                continue;
+                            // child box: lower half [lo, mid] or upper half [mid, hi] along D
+                            const iv::Box bx { clo[ch][0], (D == 0 && !ch) ? mid : __dadd_rn(tlo, wt),
+                                               clo[ch][1], (D == 1 && !ch) ? mid : __dadd_rn(ulo, wu),
+                                               clo[ch][2], (D == 2 && !ch) ? mid : __dadd_rn(vlo, wv) };
+                            const iv::Outcome e = iv::process_exact<iv::SmemPts>(vf, P, bx, t_star, sep, a.cfg);
+                            o.act[ch] = e.act;
+                            o.cand[ch] = e.cand;
+                            o.zdiag[ch] = e.zdiag;
+                            o.dim[ch] = e.dim;
+                            o.evaluated[ch] = e.evaluated;
+                        }
+                    }
+                    const unsigned long long dpc = dp + (1ull << (16 * D));
+                    unsigned counted = 0;
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch) {
+                        evals += o.evaluated[ch];
+                        if (o.act[ch] == iv::kCollision) {
+                            record_collision(a, q, o.cand[ch], o.zdiag[ch]);
+                        } else if (o.act[ch] == iv::kSplit) {
+                            ++split_actions;
+                            counted += !(a.cfg.no_zero_toi && clo[ch][0] == 0.0);
+                            r[ch] = { o.dim[ch], clo[ch][0], clo[ch][1], clo[ch][2], dpc };
+                        }
+                    }
+                    // split budget (narrowphase.cpp:254-271): requests old ..
+                    // old+counted-1; any index >= max_splits exhausts the query
+                    if (counted) {
+                        const unsigned long long old = atomicAdd(&a.splits[q], static_cast<unsigned long long>(counted));
+                        if (old + counted > a.max_splits)
+                            a.exh_gen[q] = gen;
+                    }
                 }
             }
         }
-        // children of the previous batch (their atomics have had a whole
-        // evaluation to return), then this batch's requests
-        finish_pending(a, nb, lane, gen, pend);
-        Pending np;
-        np.counted = admit && !(a.cfg.no_zero_toi && tlo == 0.0);
-        np.split_old = np.counted ? atom_add_u64(&a.splits[q], 1ull) : 0ull;
-        np.collided = collided;
-        np.dirty_slot = collided ? atom_add_u64(&sc->dirty_n + a.zero * lane, 1ull) : 0ull;
-        np.mask = __ballot_sync(0xffffffffu, admit);
-        np.leader = np.mask ? __ffs(np.mask) - 1 : 0;
-        np.slot_raw = 0;
-        if (np.mask && lane == static_cast<unsigned>(np.leader))
-            np.slot_raw = atom_add_u64(&sc->next_n + a.zero * lane, 2ull * __popc(np.mask));
-        np.dp = dp;
-        np.tlo = tlo;
-        np.ulo = ulo;
-        np.vlo = vlo;
-        np.q = q;
-        np.dim = dim;
-        pend = np;
-        if (kStages == 2) {
-            st ^= 1;
-        } else {
-            __syncwarp(); // every lane's evaluation has read the stage
-            issue(b + W, q_cur, 0);
-        }
+        append_splits(a, nb, lane, q, r);
+        st ^= 1;
     }
-    finish_pending(a, nb, lane, gen, pend);
     cp_async_wait<0>();
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);
@@ -381,12 +477,17 @@ __global__ void k_finish(GenArgs a)
         sc->peak = compacted;
     if (compacted > a.sem_cap)
         sc->sem_overflow = 1;
-    const unsigned long long raw_next = sc->next_n;
-    if (raw_next > a.phys_cap)
-        sc->phys_overflow = 1;
+    unsigned long long raw_next = 0;
+    for (int d = 0; d < 3; ++d) {
+        const unsigned long long r = sc->next_pairs[d];
+        raw_next += r;
+        if (r > a.cap_pairs)
+            sc->phys_overflow = 1;
+        sc->cur_pairs[d] = r > a.cap_pairs ? a.cap_pairs : r;
+        sc->next_pairs[d] = 0;
+    }
     sc->gen += 1;
-    sc->cur_n = raw_next > a.phys_cap ? a.phys_cap : raw_next;
-    sc->next_n = 0;
+    sc->cur_n = 2 * (sc->cur_pairs[0] + sc->cur_pairs[1] + sc->cur_pairs[2]);
     sc->dirty_n = 0;
     sc->dropped = 0;
     sc->finish_ticket = 0;
@@ -405,9 +506,7 @@ __global__ void k_finish(GenArgs a)
 __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const double* pts,
                                uint32_t* qf, unsigned long long* toi,
                                unsigned long long* snap, unsigned long long* splits,
-                               unsigned* exh_gen, uint8_t* zdiag,
-                               uint32_t* qid, double* t, double* u, double* v,
-                               unsigned long long* dep)
+                               unsigned* exh_gen, uint8_t* zdiag)
 {
     for (unsigned long long q = blockIdx.x * blockDim.x + threadIdx.x; q < n;
          q += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
@@ -416,13 +515,8 @@ __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const 
         splits[q] = 0;
         exh_gen[q] = kNoGen;
         zdiag[q] = 0;
-        qid[q] = static_cast<uint32_t>(q); // one root box [0,1]^3 per query
         qf[q] = static_cast<uint32_t>((kind[q] == CCDK_QUERY_EE ? iv::kKindEE : 0)
                                      | (iv::fast_ok(iv::GlobalPts { pts + 24 * q }) ? 0 : iv::kKindExact));
-        t[q] = 0.0;
-        u[q] = 0.0;
-        v[q] = 0.0;
-        dep[q] = 0;
     }
 }
 
@@ -600,18 +694,20 @@ T* grow(DevBuf& b, uint64_t n)
     return static_cast<T*>(b.ensure(n * sizeof(T)));
 }
 
-// Build (or reuse) the generation graph: WHILE(cond) { k_generation; k_finish }.
+// Build (or reuse) the generation graph:
+//   k_gen0 -> k_finish -> WHILE(cond) { k_generation -> k_finish }.
 // The condition defaults to 1 at every launch; k_finish clears it.
-void launch_generations(Ctx& c, GenArgs& a, unsigned gen_grid, unsigned fin_grid)
+void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_grid, unsigned fin_grid)
 {
     GenGraph& G = c.gen_graph;
     struct Key {
         GenArgs a;
-        unsigned gen_grid, fin_grid;
+        unsigned gen0_grid, gen_grid, fin_grid;
     } key;
     std::memset(&key, 0, sizeof key);
     key.a = a;
     key.a.cond = 0;
+    key.gen0_grid = gen0_grid;
     key.gen_grid = gen_grid;
     key.fin_grid = fin_grid;
     static_assert(sizeof(Key) <= sizeof(G.key), "graph key too large");
@@ -623,17 +719,30 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen_grid, unsigned fin_grid
     CCDK_CUDA_CHECK(cudaGraphCreate(&G.graph, 0));
     cudaGraphConditionalHandle h;
     CCDK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, G.graph, 1, cudaGraphCondAssignDefault));
+    GenArgs a0 = a; // generation 0 and its finish run outside the loop
+    a0.cond = 0;
     a.cond = h;
+    void* params0[] = { &a0 };
+    void* params[] = { &a };
+    cudaKernelNodeParams kp {};
+    kp.func = reinterpret_cast<void*>(k_gen0);
+    kp.gridDim = dim3(gen0_grid);
+    kp.blockDim = dim3(kGenBlock);
+    kp.kernelParams = params0;
+    cudaGraphNode_t g0, f0;
+    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&g0, G.graph, nullptr, 0, &kp));
+    kp.func = reinterpret_cast<void*>(k_finish);
+    kp.gridDim = dim3(fin_grid);
+    kp.blockDim = dim3(256);
+    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&f0, G.graph, &g0, 1, &kp));
     cudaGraphNodeParams cp {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t cnode;
-    CCDK_CUDA_CHECK(cudaGraphAddNode(&cnode, G.graph, nullptr, 0, &cp));
+    CCDK_CUDA_CHECK(cudaGraphAddNode(&cnode, G.graph, &f0, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    void* params[] = { &a };
-    cudaKernelNodeParams kp {};
     kp.func = reinterpret_cast<void*>(k_generation);
     kp.gridDim = dim3(gen_grid);
     kp.blockDim = dim3(kGenBlock);
@@ -658,6 +767,9 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
               const double* sep, double* toi_out, uint8_t* flags_out, ccdk_narrow_stats& st)
 {
     cudaStream_t s = c.stream;
+    // interval capacity per generation; stored as split records (2 intervals
+    // each) in 3 regions that may each have to hold all of them
+    constexpr uint64_t kBytesPerInterval = 3 * 36 / 2 * 2; // 3 regions x record / 2 x double buffer
     uint64_t cap = c.interval_capacity;
     if (cap == 0) {
         // size from free memory, probed once per query count (cudaMemGetInfo
@@ -665,11 +777,12 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         if (c.mem_probe_n == 0 || n > c.mem_probe_n) {
             size_t free_b = 0, total_b = 0;
             CCDK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-            // already-allocated interval buffers count as available
-            size_t held = 0;
+            size_t held = 0; // already-allocated record buffers count as available
             for (int b = 0; b < 2; ++b)
-                held += c.iv_qid[b].cap + c.iv_t[b].cap + c.iv_u[b].cap + c.iv_v[b].cap + c.iv_dep[b].cap;
-            c.mem_probe_cap = static_cast<uint64_t>((free_b + held) / 2) / 72;
+                for (int d = 0; d < 3; ++d)
+                    held += c.iv_qid[b][d].cap + c.iv_t[b][d].cap + c.iv_u[b][d].cap + c.iv_v[b][d].cap
+                        + c.iv_dep[b][d].cap;
+            c.mem_probe_cap = static_cast<uint64_t>((free_b + held) / 2) / kBytesPerInterval;
             c.mem_probe_n = n;
         }
         cap = std::max<uint64_t>(4 * n, uint64_t(1) << 24);
@@ -678,6 +791,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     }
     if (cap < n)
         return false;
+    const uint64_t cap_pairs = std::max<uint64_t>(cap / 2, 1);
     GenArgs a {};
     a.kind = kind;
     a.qf = grow<uint32_t>(c.q_flags, n);
@@ -694,26 +808,28 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     a.dirty = grow<unsigned>(c.dirty, 2 * n);
     a.dirty_cap = 2 * n;
     a.nq = n;
-    for (int b = 0; b < 2; ++b) {
-        a.qid[b] = grow<uint32_t>(c.iv_qid[b], cap);
-        a.t[b] = grow<double>(c.iv_t[b], cap);
-        a.u[b] = grow<double>(c.iv_u[b], cap);
-        a.v[b] = grow<double>(c.iv_v[b], cap);
-        a.dep[b] = grow<unsigned long long>(c.iv_dep[b], cap);
-    }
-    a.phys_cap = cap;
+    for (int b = 0; b < 2; ++b)
+        for (int d = 0; d < 3; ++d) {
+            Region& R = a.reg[b][d];
+            R.qid = grow<uint32_t>(c.iv_qid[b][d], cap_pairs);
+            R.t = grow<double>(c.iv_t[b][d], cap_pairs);
+            R.u = grow<double>(c.iv_u[b][d], cap_pairs);
+            R.v = grow<double>(c.iv_v[b][d], cap_pairs);
+            R.dep = grow<unsigned long long>(c.iv_dep[b][d], cap_pairs);
+        }
+    a.cap_pairs = cap_pairs;
     a.sem_cap = in.queue_capacity;
     a.sc = static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars)));
 
-    NarrowScalars init {};
-    init.cur_n = n;
-    init.cont = 1;
-    init.global_toi_bits = kInfBits;
-    CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    NarrowScalars* init = static_cast<NarrowScalars*>(c.pin_init.ensure(sizeof(NarrowScalars)));
+    std::memset(init, 0, sizeof(NarrowScalars));
+    init->cur_n = n;
+    init->cont = 1;
+    init->global_toi_bits = kInfBits;
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, init, sizeof(NarrowScalars), cudaMemcpyHostToDevice, s));
     const dim3 ig = grid_for(n, 256);
-    k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(
-        n, kind, pts, a.qf, a.toi, a.snap, a.splits, a.exh_gen, a.zdiag, a.qid[0], a.t[0], a.u[0],
-        a.v[0], a.dep[0]);
+    k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(n, kind, pts, a.qf, a.toi, a.snap,
+                                                                   a.splits, a.exh_gen, a.zdiag);
     CCDK_LAUNCH_CHECK();
 
     if (c.gen_blocks_per_sm == 0) {
@@ -724,16 +840,20 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         c.gen_blocks_per_sm = std::max(1, c.gen_blocks_per_sm);
     }
     const unsigned gen_grid = static_cast<unsigned>(c.gen_blocks_per_sm * c.num_sms);
+    const unsigned gen0_grid = static_cast<unsigned>(std::min<uint64_t>((n + kGenBlock - 1) / kGenBlock,
+                                                                        uint64_t(8) * c.num_sms));
     const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
 
     static const bool no_graph = std::getenv("CCDK_NO_GRAPH") != nullptr;
     if (!no_graph) {
-        launch_generations(c, a, gen_grid, fin_grid);
+        launch_generations(c, a, gen0_grid, gen_grid, fin_grid);
     } else {
         // direct launches (profilers cannot see kernel nodes under a
         // conditional node): batches of 8 generations, then a host check
         a.cond = 0;
         NarrowScalars* hs = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
+        k_gen0<<<gen0_grid, kGenBlock, 0, s>>>(a);
+        k_finish<<<fin_grid, 256, 0, s>>>(a);
         for (;;) {
             for (int g = 0; g < 8; ++g) {
                 k_generation<<<gen_grid, kGenBlock, kGenSmem, s>>>(a);
@@ -754,12 +874,16 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
                 break;
         }
     }
-    c.narrow_launches += 2; // counted below from the generation count
-
+    // per-query outputs right behind the generations (discarded on a
+    // physical overflow, when the caller halves), then one read-back
+    k_outputs<<<std::min<unsigned>(ig.x, 4096u), 256, 0, s>>>(n, a.toi, a.splits, a.exh_gen,
+                                                              a.zdiag, a.max_splits, a.sc,
+                                                              toi_out, flags_out);
+    CCDK_LAUNCH_CHECK();
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
     CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
     CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
-    c.narrow_launches += 2 * host_sc->gen - 2;
+    c.narrow_launches += 3 + 2 * host_sc->gen;
     if (debug_enabled())
         fprintf(stderr, "[ccdk narrow] n=%llu gen=%llu peak=%llu evals=%llu splits=%llu phys=%llu sem=%llu\n",
                 (unsigned long long)n, host_sc->gen, host_sc->peak, host_sc->evaluations,
@@ -768,12 +892,6 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         throw Error(CCDK_CUDA, "narrow phase: generation limit exceeded (internal error)");
     if (host_sc->phys_overflow)
         return false;
-    k_outputs<<<std::min<unsigned>(ig.x, 4096u), 256, 0, s>>>(n, a.toi, a.splits, a.exh_gen,
-                                                              a.zdiag, a.max_splits, a.sc,
-                                                              toi_out, flags_out);
-    CCDK_LAUNCH_CHECK();
-    CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
-    CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
     st.overflow = host_sc->sem_overflow ? 1 : 0;
     const double g = __builtin_bit_cast(double, static_cast<uint64_t>(host_sc->global_toi_bits));
     st.global_toi = st.overflow ? INFINITY : std::min(st.global_toi, g);

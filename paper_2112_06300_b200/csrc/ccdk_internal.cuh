@@ -199,6 +199,8 @@ struct NarrowScalars {
     unsigned long long any_flags;   // OR of per-query flags
     unsigned long long vf_count;
     unsigned long long gen_limit;   // set when the generation guard trips
+    unsigned long long cur_pairs[3];  // split records per region in the current generation
+    unsigned long long next_pairs[3]; // append cursors of the next generation
 };
 
 // The narrow phase's generation loop as one CUDA graph: a WHILE conditional
@@ -330,7 +332,8 @@ struct Ctx {
 
     // queries / narrow phase
     DevBuf q_kind, q_points, q_sep, q_flags;
-    DevBuf iv_qid[2], iv_t[2], iv_u[2], iv_v[2], iv_dep[2];
+    // interval records by split dimension (region) and generation parity
+    DevBuf iv_qid[2][3], iv_t[2][3], iv_u[2][3], iv_v[2][3], iv_dep[2][3];
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
     DevBuf nscal;                      // NarrowScalars
     GenGraph gen_graph;
@@ -348,6 +351,7 @@ struct Ctx {
     // staging for API calls
     DevBuf tmp[8];
     PinnedBuf pin;
+    PinnedBuf pin_init;                // narrow-phase scalars upload (outlives the async copy)
 
     // last step results
     DevBuf last_toi;                   // double

@@ -285,6 +285,192 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
     return kSplit;
 }
 
+// ---------------------------------------------------------------- pairs
+// The two children of a split along dimension D are evaluated together: they
+// share the parent's samples in the other two dimensions and the midpoint in
+// D, so the corner values F(t, u, v) on the shared face (and, for a u- or
+// v-split, every point position P(t) and the base/du/dv terms) are formed
+// once.  Every corner value is produced by exactly the operations of
+// evaluate_box (narrowphase.cpp:35-85) on exactly the same operands, so each
+// child's hull and influences are bit-identical to evaluating it alone; the
+// hull folds a child's corners starting from its corner 0 like the
+// reference, and in the Fast path (no NaN) min/max are order-independent.
+// Samples: dim D holds (lo, mid, hi), the others (lo, hi); child 0 takes
+// indices {0, 1} along D, child 1 {1, 2}.
+struct PairBox {
+    double t[3], u[3], v[3];
+};
+
+template <int D, class Pts>
+__device__ __forceinline__ void component_pair(bool vf, const Pts& P, const PairBox& b, int c, I rng[2],
+                                               double infl[2][3])
+{
+    using W = Fast;
+    constexpr int NT = D == 0 ? 3 : 2, NU = D == 1 ? 3 : 2, NV = D == 2 ? 3 : 2;
+    double x0[4];
+    I dl[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        x0[p] = P(3 * p + c);
+        const double x1 = P(12 + 3 * p + c);
+        const double d = __dsub_rn(x1, x0[p]);
+        dl[p] = { W::dn(d), W::up(d) };
+    }
+    double mp[NU * NV]; // corner midpoints at the previous t sample
+#pragma unroll
+    for (int it = 0; it < NT; ++it) {
+        const double t = b.t[it];
+        I at[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const I s = scale<W>(t, dl[p]);
+            at[p] = { W::dn(__dadd_rn(x0[p], s.lo)), W::up(__dadd_rn(x0[p], s.hi)) };
+        }
+        const I a_org = vf ? at[1] : at[2];
+        const I a_uto = vf ? at[2] : at[1];
+        const I a_ufr = vf ? at[1] : at[0];
+        const I base = sub<W>(at[0], a_org);
+        const I du = sub<W>(a_uto, a_ufr);
+        const I dv = sub<W>(at[3], a_org);
+        I su[NU], vt[NV];
+#pragma unroll
+        for (int iu = 0; iu < NU; ++iu) {
+            const I ut = scale<W>(b.u[iu], du);
+            su[iu] = vf ? sub<W>(base, ut) : add<W>(base, ut);
+        }
+#pragma unroll
+        for (int iv = 0; iv < NV; ++iv)
+            vt[iv] = scale<W>(b.v[iv], dv);
+        double m[NU * NV];
+#pragma unroll
+        for (int iu = 0; iu < NU; ++iu) {
+#pragma unroll
+            for (int iv = 0; iv < NV; ++iv) {
+                const I f = sub<W>(su[iu], vt[iv]);
+                m[iu * NV + iv] = mid2(f);
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int kd = D == 0 ? it : D == 1 ? iu : iv; // index along D
+                    if (kd == ch || kd == ch + 1) {
+                        const bool first = (D == 0 ? it == ch : it == 0) && (D == 1 ? iu == ch : iu == 0)
+                            && (D == 2 ? iv == ch : iv == 0);
+                        if (first) {
+                            rng[ch] = f;
+                        } else {
+                            rng[ch].lo = smin(rng[ch].lo, f.lo);
+                            rng[ch].hi = smax(rng[ch].hi, f.hi);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+            if (D == 0 && !(it == ch || it == ch + 1))
+                continue;
+            const int u0 = D == 1 ? ch : 0, v0 = D == 2 ? ch : 0;
+            // u influence: corner pairs differing in u (narrowphase.cpp:89-107)
+#pragma unroll
+            for (int iv = v0; iv < v0 + 2; ++iv)
+                infl[ch][1] = smax(infl[ch][1], fabs(__dsub_rn(m[(u0 + 1) * NV + iv], m[u0 * NV + iv])));
+            // v influence
+#pragma unroll
+            for (int iu = u0; iu < u0 + 2; ++iu)
+                infl[ch][2] = smax(infl[ch][2], fabs(__dsub_rn(m[iu * NV + v0 + 1], m[iu * NV + v0])));
+            // t influence: this t sample against the previous one
+            const bool tpair = D == 0 ? it == ch + 1 : it == 1;
+            if (tpair) {
+#pragma unroll
+                for (int iu = u0; iu < u0 + 2; ++iu)
+#pragma unroll
+                    for (int iv = v0; iv < v0 + 2; ++iv)
+                        infl[ch][0] = smax(infl[ch][0], fabs(__dsub_rn(m[iu * NV + iv], mp[iu * NV + iv])));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NU * NV; ++k)
+            mp[k] = m[k];
+    }
+}
+
+struct PairOutcome {
+    double cand[2];
+    int act[2], dim[2];
+    bool zdiag[2], evaluated[2];
+};
+
+// process_interval (narrowphase.cpp:134-187) on both children of a pair
+// (Fast widening only).  `alive[ch]` is false for a child the caller has
+// already pruned by t >= t*, t >= t_max or the VF simplex test.
+template <int D, class Pts>
+__device__ __forceinline__ PairOutcome process_pair(bool vf, const Pts& P, const PairBox& b, const bool alive0[2],
+                                                    double d, const Cfg& cfg)
+{
+    PairOutcome o;
+    bool alive[2] = { alive0[0], alive0[1] };
+    bool inside[2] = { true, true };
+    double wmax[2] = { 0.0, 0.0 };
+    double infl[2][3] = { { 0.0, 0.0, 0.0 }, { 0.0, 0.0, 0.0 } };
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+        o.act[ch] = kPruned;
+        o.dim[ch] = -1;
+        o.zdiag[ch] = false;
+        o.evaluated[ch] = alive[ch];
+        o.cand[ch] = 0.0;
+    }
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        I rng[2];
+        component_pair<D, Pts>(vf, P, b, c, rng, infl);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+            if (rng[ch].lo > d || rng[ch].hi < -d)
+                alive[ch] = false;
+            inside[ch] = inside[ch] && rng[ch].lo >= -d && rng[ch].hi <= d;
+            const double w = __dsub_rn(rng[ch].hi, rng[ch].lo);
+            wmax[ch] = c == 0 ? w : smax(wmax[ch], w);
+        }
+        if (!alive[0] && !alive[1])
+            return o;
+    }
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+        if (!alive[ch])
+            continue;
+        const double tlo = b.t[D == 0 ? ch : 0], thi = b.t[D == 0 ? ch + 1 : 1];
+        const double ulo = b.u[D == 1 ? ch : 0], uhi = b.u[D == 1 ? ch + 1 : 1];
+        const double vlo = b.v[D == 2 ? ch : 0], vhi = b.v[D == 2 ? ch + 1 : 1];
+        const bool force_zero = cfg.no_zero_toi && tlo == 0.0;
+        if (!force_zero && (wmax[ch] < cfg.delta || inside[ch])) {
+            o.cand[ch] = tlo;
+            o.act[ch] = kCollision;
+            continue;
+        }
+        int dim = -1;
+        double best = 0.0;
+        if (splittable(tlo, thi)) {
+            dim = 0;
+            best = infl[ch][0];
+        }
+        if (splittable(ulo, uhi) && (dim < 0 || infl[ch][1] > best)) {
+            dim = 1;
+            best = infl[ch][1];
+        }
+        if (splittable(vlo, vhi) && (dim < 0 || infl[ch][2] > best))
+            dim = 2;
+        if (dim < 0) {
+            o.cand[ch] = tlo;
+            o.zdiag[ch] = force_zero;
+            o.act[ch] = kCollision;
+        } else {
+            o.dim[ch] = dim;
+            o.act[ch] = kSplit;
+        }
+    }
+    return o;
+}
+
 // A query takes the Fast widening when every coordinate is <= 2^1000 in
 // magnitude (see the header comment).
 // The Exact-widening instantiation is out of line: it runs only for queries
