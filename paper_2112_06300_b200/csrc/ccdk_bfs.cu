@@ -231,22 +231,33 @@ struct BatchLoc {
     unsigned long long n;     // records in the region
 };
 
-__device__ __forceinline__ BatchLoc locate(const unsigned long long nbr[3], const unsigned long long cnt[3],
-                                           unsigned long long b)
+// Batch b of the concatenated region batch space (regions padded to whole
+// batches so a batch's split dimension is warp-uniform).  Scalar selects, no
+// runtime-indexed arrays (those would live in local memory).
+__device__ __forceinline__ BatchLoc locate(unsigned long long nb0, unsigned long long nb1,
+                                           unsigned long long c0, unsigned long long c1,
+                                           unsigned long long c2, unsigned long long b)
 {
     BatchLoc L;
-    if (b < nbr[0]) {
+    if (b < nb0) {
         L.d = 0;
-    } else if (b < nbr[0] + nbr[1]) {
+        L.n = c0;
+    } else if (b < nb0 + nb1) {
         L.d = 1;
-        b -= nbr[0];
+        L.n = c1;
+        b -= nb0;
     } else {
         L.d = 2;
-        b -= nbr[0] + nbr[1];
+        L.n = c2;
+        b -= nb0 + nb1;
     }
     L.i0 = b << 5;
-    L.n = cnt[L.d];
     return L;
+}
+
+__device__ __forceinline__ const Region& region(const GenArgs& a, int par, int d)
+{
+    return d == 0 ? a.reg[par][0] : d == 1 ? a.reg[par][1] : a.reg[par][2];
 }
 
 template <int D>
@@ -264,13 +275,9 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
         return;
     const unsigned gen = static_cast<unsigned>(sc->gen);
     const int cb = gen & 1, nb = cb ^ 1;
-    unsigned long long cnt[3], nbr[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        cnt[d] = sc->cur_pairs[d];
-        nbr[d] = (cnt[d] + 31) >> 5;
-    }
-    const unsigned long long nbatch = nbr[0] + nbr[1] + nbr[2];
+    const unsigned long long c0 = sc->cur_pairs[0], c1 = sc->cur_pairs[1], c2 = sc->cur_pairs[2];
+    const unsigned long long nb0 = (c0 + 31) >> 5, nb1 = (c1 + 31) >> 5, nb2 = (c2 + 31) >> 5;
+    const unsigned long long nbatch = nb0 + nb1 + nb2;
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
     double* stage0 = gsm + wib * kWarpSmemDoubles;
@@ -285,10 +292,10 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     auto issue = [&](unsigned long long bb, unsigned q, int st) {
         // batch bb's coordinates + record + query scalars, batch bb+W's ids
         if (bb < nbatch) {
-            const BatchLoc L = locate(nbr, cnt, bb);
+            const BatchLoc L = locate(nb0, nb1, c0, c1, c2, bb);
             const unsigned long long i = L.i0 + lane;
             if (i < L.n) {
-                const Region& R = a.reg[cb][L.d];
+                const Region& R = region(a, cb, L.d);
                 double* coords = stage0 + st * kStageDoubles;
                 const double* src = a.pts + 24ull * q;
 #pragma unroll
@@ -307,26 +314,30 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
             }
         }
         if (bb + W < nbatch) {
-            const BatchLoc L = locate(nbr, cnt, bb + W);
+            const BatchLoc L = locate(nb0, nb1, c0, c1, c2, bb + W);
             const unsigned long long i = L.i0 + lane;
             if (i < L.n)
-                cp_async4(qbuf + lane, a.reg[cb][L.d].qid + i);
+                cp_async4(qbuf + lane, region(a, cb, L.d).qid + i);
         }
         cp_async_commit();
     };
 
+    // split-budget request of the previous batch: its atomic's old value is
+    // consumed one batch later (the round trip overlaps this batch)
+    unsigned long long bud_old = 0;
+    unsigned bud_cnt = 0, bud_q = 0;
     unsigned q_cur;
     {
-        const BatchLoc L = locate(nbr, cnt, b);
+        const BatchLoc L = locate(nb0, nb1, c0, c1, c2, b);
         const unsigned long long i = L.i0 + lane;
-        q_cur = i < L.n ? a.reg[cb][L.d].qid[i] : 0u;
+        q_cur = i < L.n ? region(a, cb, L.d).qid[i] : 0u;
     }
     issue(b, q_cur, 0);
     int st = 0;
 
     for (; b < nbatch; b += W) {
         cp_async_wait<0>(); // batch b's data and batch b+W's ids (issued one batch ago)
-        const BatchLoc L = locate(nbr, cnt, b);
+        const BatchLoc L = locate(nb0, nb1, c0, c1, c2, b);
         const bool valid = L.i0 + lane < L.n;
         const unsigned q = q_cur;
         const double tlo = meta[32 * kMT + lane];
@@ -343,6 +354,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
 
         SplitRec r[2];
         r[0].dim = r[1].dim = -1;
+        unsigned req = 0;
         if (valid) {
             const int D = L.d;
             if (exh < gen) {
@@ -413,7 +425,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                         }
                     }
                     const unsigned long long dpc = dp + (1ull << (16 * D));
-                    unsigned counted = 0;
+                    unsigned counted = 0; // budget-counted split requests of the pair
 #pragma unroll
                     for (int ch = 0; ch < 2; ++ch) {
                         evals += o.evaluated[ch];
@@ -425,19 +437,30 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                             r[ch] = { o.dim[ch], clo[ch][0], clo[ch][1], clo[ch][2], dpc };
                         }
                     }
-                    // split budget (narrowphase.cpp:254-271): requests old ..
-                    // old+counted-1; any index >= max_splits exhausts the query
-                    if (counted) {
-                        const unsigned long long old = atomicAdd(&a.splits[q], static_cast<unsigned long long>(counted));
-                        if (old + counted > a.max_splits)
-                            a.exh_gen[q] = gen;
-                    }
+                    req = counted;
                 }
             }
         }
+        // split budget (narrowphase.cpp:254-271): this pair's requests are
+        // old .. old+req-1 and any index >= max_splits exhausts the query;
+        // the old value is checked one batch later
+        if (bud_cnt && bud_old + bud_cnt > a.max_splits)
+            a.exh_gen[bud_q] = gen;
+        bud_cnt = req;
+        bud_q = q;
+        // predicated PTX atomic with the loop-carried register as its
+        // destination ("+l"): a C++ atomicAdd under `if` makes the compiler
+        // copy the result into that register right away, i.e. wait for it
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+                     "@p atom.global.add.u64 %0, [%1], %2;\n\t}"
+                     : "+l"(bud_old)
+                     : "l"(a.splits + q), "l"(static_cast<unsigned long long>(req)), "r"(req)
+                     : "memory");
         append_splits(a, nb, lane, q, r);
         st ^= 1;
     }
+    if (bud_cnt && bud_old + bud_cnt > a.max_splits)
+        a.exh_gen[bud_q] = gen;
     cp_async_wait<0>();
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);
