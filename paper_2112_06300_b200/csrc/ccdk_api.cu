@@ -436,8 +436,9 @@ struct BatchRun {
         CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
         uint8_t* qk = grow<uint8_t>(c.q_kind, std::max<uint64_t>(n, 1));
         double* qp = grow<double>(c.q_points, 24 * std::max<uint64_t>(n, 1));
+        uint32_t* qfl = grow<uint32_t>(c.q_pflags, std::max<uint64_t>(n, 1));
         launch_classify_keys(c, keys, n, c.last_nb, s.v0.as<double>(), s.v1.as<double>(), s.nv,
-                             s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp);
+                             s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp, qfl);
         double* seps = nullptr;
         if (cfg.min_sep_mode == CCDK_MINSEP_RELATIVE && n) {
             seps = grow<double>(c.q_sep, n);
@@ -458,7 +459,7 @@ struct BatchRun {
         queries += n;
         grow_results(queries);
         if (n)
-            narrow_batch(qk, qp, seps, 0, n, qoff);
+            narrow_batch(qk, qp, seps, qfl, 0, n, qoff);
         else
             ++narrow_batches; // an empty narrow run still counts as a batch
         CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
@@ -476,8 +477,8 @@ struct BatchRun {
 
     // narrow_batch (pipeline.cpp:103-138): queue capacity from the budget,
     // halve the queries on overflow
-    void narrow_batch(const uint8_t* qk, const double* qp, const double* seps, uint64_t lo,
-                      uint64_t hi, uint64_t qoff)
+    void narrow_batch(const uint8_t* qk, const double* qp, const double* seps, const uint32_t* qfl,
+                      uint64_t lo, uint64_t hi, uint64_t qoff)
     {
         const uint64_t n_sub = hi - lo;
         const uint64_t pair_bytes = n_sub * (cfg.rs_query + 3 * cfg.rs_pair_ints);
@@ -488,6 +489,7 @@ struct BatchRun {
         ni.kind = qk + lo;
         ni.points = qp + 24 * lo;
         ni.sep = seps ? seps + lo : nullptr;
+        ni.qflags = qfl ? qfl + lo : nullptr;
         ni.n = n_sub;
         ni.cfg = cfg.narrow;
         ni.queue_capacity = avail / cfg.rs_interval;
@@ -499,8 +501,8 @@ struct BatchRun {
             if (n_sub <= 1)
                 throw Error(CCDK_CONFIG, "memory budget too small to hold even one query");
             const uint64_t mid = lo + n_sub / 2;
-            narrow_batch(qk, qp, seps, lo, mid, qoff);
-            narrow_batch(qk, qp, seps, mid, hi, qoff);
+            narrow_batch(qk, qp, seps, qfl, lo, mid, qoff);
+            narrow_batch(qk, qp, seps, qfl, mid, hi, qoff);
             return;
         }
         ++narrow_batches;

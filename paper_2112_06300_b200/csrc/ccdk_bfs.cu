@@ -526,6 +526,14 @@ __global__ void k_finish(GenArgs a)
         cudaGraphSetConditional(a.cond, sc->cont ? 1u : 0u);
 }
 
+__device__ __forceinline__ uint32_t query_flags(uint8_t kind, const double* pts)
+{
+    return static_cast<uint32_t>((kind == CCDK_QUERY_EE ? iv::kKindEE : 0)
+                                 | (iv::fast_ok(iv::GlobalPts { pts }) ? 0 : iv::kKindExact));
+}
+
+// qf == nullptr: the flags were precomputed (classify) and are not rebuilt,
+// which saves reading every query record once more.
 __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const double* pts,
                                uint32_t* qf, unsigned long long* toi,
                                unsigned long long* snap, unsigned long long* splits,
@@ -538,8 +546,8 @@ __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const 
         splits[q] = 0;
         exh_gen[q] = kNoGen;
         zdiag[q] = 0;
-        qf[q] = static_cast<uint32_t>((kind[q] == CCDK_QUERY_EE ? iv::kKindEE : 0)
-                                     | (iv::fast_ok(iv::GlobalPts { pts + 24 * q }) ? 0 : iv::kKindExact));
+        if (qf)
+            qf[q] = query_flags(kind[q], pts + 24 * q);
     }
 }
 
@@ -651,42 +659,65 @@ __global__ void k_process(const uint8_t* kind, const double* pts, const double* 
 // Canonical keys list every VF pair (left = vertex) before every EE pair
 // (left = edge), which is the pipeline's VF-then-EE order
 // (pipeline.cpp:162-165); all pairs already passed keep_pair in the sweep.
-__global__ void k_classify_keys(const unsigned long long* keys, unsigned long long n, int nb,
-                                const double* __restrict__ v0, const double* __restrict__ v1,
-                                unsigned long long nv, const uint32_t* __restrict__ e,
-                                unsigned long long ne, const uint32_t* __restrict__ f,
-                                uint8_t* kind, double* pts)
+// One warp per 32 consecutive queries: gathers in registers, then the
+// warp's 32 contiguous 192-byte records (6 KiB) are written through shared
+// memory as coalesced 256-byte rows; the query flags (kind | exact-widening,
+// iv::kKind*) are produced here so the narrow phase need not re-read the
+// records to derive them.
+constexpr int kClassifyBlock = 128;
+
+__global__ void __launch_bounds__(kClassifyBlock) k_classify_keys(
+    const unsigned long long* keys, unsigned long long n, int nb, const double* __restrict__ v0,
+    const double* __restrict__ v1, unsigned long long nv, const uint32_t* __restrict__ e,
+    unsigned long long ne, const uint32_t* __restrict__ f, uint8_t* kind, double* pts,
+    uint32_t* qflags)
 {
+    __shared__ double stage[kClassifyBlock / 32][32 * 24];
+    const unsigned lane = threadIdx.x & 31;
+    double* st = stage[threadIdx.x >> 5];
     const unsigned long long q = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
-    if (q >= n)
-        return;
-    const unsigned long long key = keys[q];
-    const unsigned long long lo = key >> nb;
-    const unsigned long long hi = key & ((1ull << nb) - 1);
-    uint32_t pv[4];
-    if (lo < nv) { // vertex-face: (p, t0, t1, t2)
-        const unsigned long long fi = hi - nv - ne;
-        pv[0] = static_cast<uint32_t>(lo);
-        pv[1] = f[3 * fi];
-        pv[2] = f[3 * fi + 1];
-        pv[3] = f[3 * fi + 2];
-        kind[q] = CCDK_QUERY_VF;
-    } else { // edge-edge: (e0a, e0b, e1a, e1b)
-        const unsigned long long ea = lo - nv, eb = hi - nv;
-        pv[0] = e[2 * ea];
-        pv[1] = e[2 * ea + 1];
-        pv[2] = e[2 * eb];
-        pv[3] = e[2 * eb + 1];
-        kind[q] = CCDK_QUERY_EE;
-    }
-    double* out = pts + 24 * q;
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            out[3 * p + c] = v0[3ull * pv[p] + c];
-            out[12 + 3 * p + c] = v1[3ull * pv[p] + c];
+    const unsigned long long q0 = q - lane; // first query of the warp
+    if (q0 >= n)
+        return; // warp-uniform
+    if (q < n) {
+        const unsigned long long key = keys[q];
+        const unsigned long long lo = key >> nb;
+        const unsigned long long hi = key & ((1ull << nb) - 1);
+        uint32_t pv[4];
+        uint8_t k;
+        if (lo < nv) { // vertex-face: (p, t0, t1, t2)
+            const unsigned long long fi = hi - nv - ne;
+            pv[0] = static_cast<uint32_t>(lo);
+            pv[1] = f[3 * fi];
+            pv[2] = f[3 * fi + 1];
+            pv[3] = f[3 * fi + 2];
+            k = CCDK_QUERY_VF;
+        } else { // edge-edge: (e0a, e0b, e1a, e1b)
+            const unsigned long long ea = lo - nv, eb = hi - nv;
+            pv[0] = e[2 * ea];
+            pv[1] = e[2 * ea + 1];
+            pv[2] = e[2 * eb];
+            pv[3] = e[2 * eb + 1];
+            k = CCDK_QUERY_EE;
         }
+        kind[q] = k;
+        bool fast = true;
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double a = v0[3ull * pv[p] + c], b = v1[3ull * pv[p] + c];
+                st[24 * lane + 3 * p + c] = a;
+                st[24 * lane + 12 + 3 * p + c] = b;
+                fast = fast && fabs(a) <= iv::kFastLimit && fabs(b) <= iv::kFastLimit;
+            }
+        qflags[q] = (k == CCDK_QUERY_EE ? iv::kKindEE : 0u) | (fast ? 0u : iv::kKindExact);
+    }
+    __syncwarp();
+    const unsigned long long valid = n - q0 < 32 ? n - q0 : 32;
+    double* out = pts + 24 * q0;
+    for (unsigned i = lane; i < 24 * valid; i += 32)
+        out[i] = st[i];
 }
 
 __global__ void k_keys_to_ids(const unsigned long long* keys, unsigned long long n, int nb,
@@ -787,7 +818,8 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_gri
 // One device run over queries [0, n) of `in`; returns false on physical
 // interval-buffer overflow (caller halves).
 bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const double* pts,
-              const double* sep, double* toi_out, uint8_t* flags_out, ccdk_narrow_stats& st)
+              const double* sep, const uint32_t* qflags, double* toi_out, uint8_t* flags_out,
+              ccdk_narrow_stats& st)
 {
     cudaStream_t s = c.stream;
     // interval capacity per generation; stored as split records (2 intervals
@@ -817,7 +849,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     const uint64_t cap_pairs = std::max<uint64_t>(cap / 2, 1);
     GenArgs a {};
     a.kind = kind;
-    a.qf = grow<uint32_t>(c.q_flags, n);
+    a.qf = qflags ? const_cast<uint32_t*>(qflags) : grow<uint32_t>(c.q_flags, n);
     a.pts = pts;
     a.sep = sep;
     a.sep_default = in.cfg.min_separation;
@@ -851,8 +883,9 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     init->global_toi_bits = kInfBits;
     CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, init, sizeof(NarrowScalars), cudaMemcpyHostToDevice, s));
     const dim3 ig = grid_for(n, 256);
-    k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(n, kind, pts, a.qf, a.toi, a.snap,
-                                                                   a.splits, a.exh_gen, a.zdiag);
+    k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(n, kind, pts, qflags ? nullptr : a.qf,
+                                                                   a.toi, a.snap, a.splits, a.exh_gen,
+                                                                   a.zdiag);
     CCDK_LAUNCH_CHECK();
 
     if (c.gen_blocks_per_sm == 0) {
@@ -934,7 +967,7 @@ void run_range(Ctx& c, const NarrowIn& in, uint64_t lo, uint64_t hi, double* toi
     if (n == 0)
         return;
     if (run_once(c, in, n, in.kind + lo, in.points + 24 * lo, in.sep ? in.sep + lo : nullptr,
-                 toi_out + lo, flags_out + lo, st))
+                 in.qflags ? in.qflags + lo : nullptr, toi_out + lo, flags_out + lo, st))
         return;
     if (n <= 1)
         throw Error(CCDK_CAPACITY, "narrow phase: interval buffer cannot hold one query's frontier");
@@ -1013,12 +1046,12 @@ void launch_process(Ctx& c, const uint8_t* kind, const double* pts, const double
 
 void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb, const double* v0,
                           const double* v1, uint64_t nv, const uint32_t* e, uint64_t ne,
-                          const uint32_t* f, uint8_t* kind, double* pts)
+                          const uint32_t* f, uint8_t* kind, double* pts, uint32_t* qflags)
 {
     if (!n)
         return;
-    k_classify_keys<<<grid_for(n, 128), 128, 0, c.stream>>>(
-        reinterpret_cast<const unsigned long long*>(keys), n, nb, v0, v1, nv, e, ne, f, kind, pts);
+    k_classify_keys<<<grid_for(n, kClassifyBlock), kClassifyBlock, 0, c.stream>>>(
+        reinterpret_cast<const unsigned long long*>(keys), n, nb, v0, v1, nv, e, ne, f, kind, pts, qflags);
     CCDK_LAUNCH_CHECK();
 }
 

@@ -269,6 +269,7 @@ struct NarrowIn {
     const uint8_t* kind = nullptr;   // device
     const double* points = nullptr;  // device, n*24
     const double* sep = nullptr;     // device or null
+    const uint32_t* qflags = nullptr; // device or null: per-query kind | exact-widening flags precomputed
     uint64_t n = 0;
     ccdk_narrow_cfg cfg {};
     uint64_t queue_capacity = UINT64_MAX;
@@ -291,7 +292,7 @@ void launch_process(Ctx& c, const uint8_t* kind, const double* pts, const double
 void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
                           const double* v0, const double* v1, uint64_t nv,
                           const uint32_t* e, uint64_t ne, const uint32_t* f, uint8_t* kind,
-                          double* pts);
+                          double* pts, uint32_t* qflags);
 // query_min_separations (pipeline.cpp:39-55) incl. the distances of
 // distance.cpp (ccdk_distance.cu)
 void launch_min_seps(Ctx& c, const uint8_t* kind, const double* pts, uint64_t n,
@@ -331,7 +332,7 @@ struct Ctx {
     bool last_pairs_general = false;
 
     // queries / narrow phase
-    DevBuf q_kind, q_points, q_sep, q_flags;
+    DevBuf q_kind, q_points, q_sep, q_flags, q_pflags;
     // interval records by split dimension (region) and generation parity
     DevBuf iv_qid[2][3], iv_t[2][3], iv_u[2][3], iv_v[2][3], iv_dep[2][3];
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
