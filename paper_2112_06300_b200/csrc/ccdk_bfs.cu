@@ -196,12 +196,11 @@ __global__ void __launch_bounds__(kGenBlock) k_gen0(GenArgs a)
                 record_collision(a, q, cand, zd);
             } else if (act == iv::kSplit) {
                 ++split_actions;
-                // t.lo == 0 here: exempt from the budget in no-zero-ToI mode
-                if (!a.cfg.no_zero_toi) {
-                    const unsigned long long old = atomicAdd(&a.splits[q], 1ull);
-                    if (old >= a.max_splits)
-                        a.exh_gen[q] = 0;
-                }
+                // t.lo == 0 here: exempt from the budget in no-zero-ToI mode.
+                // A root is its query's only request of generation 0 and
+                // max_splits >= 1, so it is always admitted (no read-back).
+                if (!a.cfg.no_zero_toi)
+                    atomicAdd(&a.splits[q], 1ull);
                 r[0] = { dim, 0.0, 0.0, 0.0, 0ull };
             }
         }
@@ -219,11 +218,11 @@ __global__ void __launch_bounds__(kGenBlock) k_gen0(GenArgs a)
 // generation | query flags), all brought in by cp.async while the previous
 // batch is evaluated; the next batch's query ids ride one batch ahead.
 constexpr int kStageDoubles = 24 * 32;
-constexpr int kMetaDoubles = 7 * 32;
+constexpr int kMetaDoubles = 8 * 32;
 constexpr int kQidDoubles = 16;
 constexpr int kWarpSmemDoubles = 2 * kStageDoubles + kMetaDoubles + kQidDoubles;
 constexpr int kGenSmem = (kGenBlock / 32) * kWarpSmemDoubles * sizeof(double);
-enum { kMT = 0, kMU, kMV, kMDep, kMSnap, kMSep, kMExh };
+enum { kMT = 0, kMU, kMV, kMDep, kMSnap, kMSep, kMExh, kMSplits };
 
 struct BatchLoc {
     int d;                    // region (split dimension)
@@ -311,6 +310,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                 unsigned* ex = reinterpret_cast<unsigned*>(meta + 32 * kMExh + lane);
                 cp_async4(ex, a.exh_gen + q);
                 cp_async4(ex + 1, a.qf + q);
+                cp_async8(meta + 32 * kMSplits + lane, a.splits + q);
             }
         }
         if (bb + W < nbatch) {
@@ -322,10 +322,9 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
         cp_async_commit();
     };
 
-    // split-budget request of the previous batch: its atomic's old value is
-    // consumed one batch later (the round trip overlaps this batch)
-    unsigned long long bud_old = 0;
-    unsigned bud_cnt = 0, bud_q = 0;
+    // every query makes at most 2 split requests per record of this
+    // generation, so at most req_bound in total this generation
+    const unsigned long long req_bound = 2 * (c0 + c1 + c2);
     unsigned q_cur;
     {
         const BatchLoc L = locate(nb0, nb1, c0, c1, c2, b);
@@ -348,6 +347,8 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
         const double sep = a.sep ? meta[32 * kMSep + lane] : a.sep_default;
         const unsigned exh = reinterpret_cast<const unsigned*>(meta + 32 * kMExh + lane)[0];
         const unsigned qf = reinterpret_cast<const unsigned*>(meta + 32 * kMExh + lane)[1];
+        const unsigned long long splits0 =
+            static_cast<unsigned long long>(__double_as_longlong(meta[32 * kMSplits + lane]));
         q_cur = qbuf[lane];
         // batch b+W streams into the other coordinate buffer while b is evaluated
         issue(b + W, q_cur, st ^ 1);
@@ -441,26 +442,24 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                 }
             }
         }
-        // split budget (narrowphase.cpp:254-271): this pair's requests are
-        // old .. old+req-1 and any index >= max_splits exhausts the query;
-        // the old value is checked one batch later
-        if (bud_cnt && bud_old + bud_cnt > a.max_splits)
-            a.exh_gen[bud_q] = gen;
-        bud_cnt = req;
-        bud_q = q;
-        // predicated PTX atomic with the loop-carried register as its
-        // destination ("+l"): a C++ atomicAdd under `if` makes the compiler
-        // copy the result into that register right away, i.e. wait for it
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
-                     "@p atom.global.add.u64 %0, [%1], %2;\n\t}"
-                     : "+l"(bud_old)
-                     : "l"(a.splits + q), "l"(static_cast<unsigned long long>(req)), "r"(req)
-                     : "memory");
+        // split budget (narrowphase.cpp:254-271): this pair's requests get
+        // indices old .. old+req-1 and any index >= max_splits exhausts the
+        // query.  splits0 (read after the generation started) + req_bound
+        // bounds every index of this generation, so below the budget no
+        // index can reach it and the count is a fire-and-forget reduction;
+        // otherwise the exact old value decides.
+        if (req) {
+            if (splits0 + req_bound <= a.max_splits) {
+                atomicAdd(&a.splits[q], static_cast<unsigned long long>(req));
+            } else {
+                const unsigned long long old = atomicAdd(&a.splits[q], static_cast<unsigned long long>(req));
+                if (old + req > a.max_splits)
+                    a.exh_gen[q] = gen;
+            }
+        }
         append_splits(a, nb, lane, q, r);
         st ^= 1;
     }
-    if (bud_cnt && bud_old + bud_cnt > a.max_splits)
-        a.exh_gen[bud_q] = gen;
     cp_async_wait<0>();
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);
