@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rebalance", choices=["auto", "on", "off"], default="auto",
+                    help="multi-GPU narrow-phase load balance by candidate count (auto: on when N > 1)")
     ap.add_argument("--c5-queries", type=int, default=10_000_000,
                     help="narrow-phase-only leg (BASELINE config 5); 0 disables")
     ap.add_argument("--c5-steps", type=int, default=3)
@@ -294,11 +296,14 @@ def run_ours(args):
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if distributed:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2112_06300_b200 import abi, ccdkit as ck, native, scenes
-    from paper_2112_06300_b200.multigpu import ShardedCcd
+    from paper_2112_06300_b200.multigpu import RebalancedCcd, ShardedCcd
+    rebalance = args.rebalance == "on" or (args.rebalance == "auto" and world > 1)
+    Step = RebalancedCcd if rebalance else ShardedCcd
 
     stream = torch.cuda.Stream()
     ctx = native.Context(local)
@@ -314,7 +319,7 @@ def run_ours(args):
 
     with torch.cuda.stream(stream):
         resident = ck.ResidentScene(scene, ctx)
-        sharded = ShardedCcd(resident, rank, world)
+        sharded = Step(resident, rank, world)
         for _ in range(args.warmup):
             flush.zero_()
             rep = sharded.step(cfg)
@@ -359,7 +364,7 @@ def run_ours(args):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 res = ck.ResidentScene(pscene, ctx)          # H2D + validation
-                sh = ShardedCcd(res, rank, world)
+                sh = Step(res, rank, world)
                 r = sh.step(cfg)                               # step + report D2H
                 sh.global_toi(r)                               # global ToI D2H
                 b.record(stream)
@@ -400,7 +405,7 @@ def run_ours(args):
             cpu = {"error": str(e)}
 
     if rank != 0:
-        if world > 1:
+        if distributed:
             torch.distributed.destroy_process_group()
         return 0
 
@@ -445,7 +450,9 @@ def run_ours(args):
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "scene": WORKLOADS[args.workload], "primitives": k,
-                   "parallelism": f"sweep-range shards x{world}, allreduce(min)",
+                   "parallelism": f"sweep-range shards x{world}"
+                                  + (", candidates rebalanced by count (all_to_all)" if rebalance else "")
+                                  + ", allreduce(min)",
                    "l2": "flushed (256 MiB memset) before every timed step"},
         "narrow_queries_per_s": queries / (narrow_ms * 1e-3) if narrow_ms > 0 else None,
         "candidates": candidates, "queries": queries, "toi": gtoi,
@@ -464,7 +471,7 @@ def run_ours(args):
         "narrow_only": c5,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
     return 0
 

@@ -258,6 +258,22 @@ CCDK_API int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1
  * shards with an allreduce(min) of report->toi. */
 CCDK_API int ccdk_ccd_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shard_rank,
                       uint32_t shard_count, ccdk_report* report);
+/* Multi-GPU rebalance: the step split at the candidate list.
+ * ccdk_broad_resident runs the box build and this shard's STQ sweep + pair
+ * sort on the uploaded scene; the shard's canonical pair keys
+ * (lo_rank << key_bits | hi_rank, u64) stay on the device; copy them out with
+ * ccdk_copy_keys_device (n_pairs * 8 bytes).  ccdk_ccd_keys_resident then
+ * classifies and narrow-phases ANY slice of such keys (device memory, any
+ * order; sorted internally): per-query results are partition-independent
+ * (narrowphase.hpp:93-96), so ranks can exchange keys to equalise counts. */
+CCDK_API int ccdk_broad_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shard_rank,
+                                 uint32_t shard_count, uint64_t* n_pairs, int* key_bits,
+                                 float* device_ms);
+CCDK_API int ccdk_copy_keys_device(ccdk_ctx* ctx, void* dst_dev);
+CCDK_API int ccdk_ccd_keys_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg,
+                                    const uint64_t* dev_keys, uint64_t n, int key_bits,
+                                    ccdk_report* report);
+
 /* Device pointer (double) holding the last step's global ToI, for a
  * device-side allreduce(min) by the multi-GPU host layer. */
 CCDK_API int ccdk_last_toi_device_ptr(ccdk_ctx* ctx, void** dev_ptr);

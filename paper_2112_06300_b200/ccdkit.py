@@ -481,6 +481,27 @@ class ResidentScene:
         check(lib().ccdk_ccd_resident(self.ctx.h, C.byref(ccfg), shard, shards, C.byref(r)))
         return _report(r, None)
 
+    def broad(self, cfg: PipelineConfig, shard: int = 0, shards: int = 1):
+        """Box build + this shard's sweep + pair sort; keys stay on the device.
+        Returns (n_pairs, key_bits, device_ms)."""
+        n, nb, ms = C.c_uint64(), C.c_int(), C.c_float()
+        ccfg = cfg.to_c()
+        check(lib().ccdk_broad_resident(self.ctx.h, C.byref(ccfg), shard, shards, C.byref(n), C.byref(nb),
+                                        C.byref(ms)))
+        return int(n.value), int(nb.value), float(ms.value)
+
+    def copy_keys(self, dev_ptr: int):
+        """Device copy of the last broad() keys (n_pairs u64) into dev_ptr."""
+        check(lib().ccdk_copy_keys_device(self.ctx.h, C.c_void_p(dev_ptr)))
+
+    def narrow_keys(self, cfg: PipelineConfig, keys_ptr: int, n: int, key_bits: int) -> CcdReport:
+        """Classify + narrow phase on n canonical pair keys in device memory."""
+        r = abi.Report()
+        ccfg = cfg.to_c()
+        check(lib().ccdk_ccd_keys_resident(self.ctx.h, C.byref(ccfg), C.c_void_p(keys_ptr), n, key_bits,
+                                           C.byref(r)))
+        return _report(r, None)
+
     def candidates(self, n: int) -> np.ndarray:
         out = np.empty((n, 2), np.uint64)
         if n:

@@ -424,8 +424,15 @@ struct BatchRun {
             return;
         }
         ++broad_batches;
-        const uint64_t n = bo.n_pairs;
-        const uint64_t* keys = c.pair_keys_sorted.as<uint64_t>();
+        process_keys(c.pair_keys_sorted.as<uint64_t>(), bo.n_pairs);
+    }
+
+    // The rest of a broad batch on canonical pair keys (lo << nb | hi over
+    // slot ranks): append them to the step's candidate list, classify
+    // (K7) + query_min_separations, narrow phase.  Also the entry for keys
+    // supplied from outside (multi-GPU rebalance).
+    void process_keys(const uint64_t* keys, uint64_t n)
+    {
         uint64_t* all = static_cast<uint64_t*>(c.all_keys.ensure_keep((candidates + n) * 8, c.stream));
         if (n)
             CCDK_CUDA_CHECK(cudaMemcpyAsync(all + candidates, keys, n * 8, cudaMemcpyDeviceToDevice, c.stream));
@@ -619,6 +626,118 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     rep.broad_batches = run.broad_batches;
     rep.t_cb = ms_build * 1e-3;
     rep.t_bp = (run.ms_sort + run.ms_sweep + run.ms_pairsort) * 1e-3;
+    rep.t_socd = run.ms_classify * 1e-3;
+    rep.t_np = run.ms_narrow * 1e-3;
+}
+
+// K1 on the resident scene (the scene was validated when it was uploaded).
+void build_resident_boxes(Ctx& c, const ccdk_pipeline_cfg& cfg, float*& bmin, float*& bmax, uint4*& vids)
+{
+    DevScene& s = c.scene;
+    const uint64_t k = s.nv + s.ne + s.nf;
+    bmin = grow<float>(c.bmin, 3 * std::max<uint64_t>(k, 1));
+    bmax = grow<float>(c.bmax, 3 * std::max<uint64_t>(k, 1));
+    vids = grow<uint4>(c.vids, std::max<uint64_t>(k, 1));
+    launch_build_boxes(c, s.v0.as<double>(), s.v1.as<double>(), s.nv, s.edges.as<uint32_t>(), s.ne,
+                       s.faces.as<uint32_t>(), s.nf, cfg.inflation, bmin, bmax, vids);
+    if (k) {
+        auto* ctr = c.counters.as<DevCounters>();
+        unsigned long long err = 0;
+        d2h(c, &err, &ctr->error, 8);
+        sync(c);
+        if (err != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
+    }
+}
+
+// Multi-GPU rebalance, first half: box build + this shard's STQ sweep + pair
+// sort; the shard's canonical keys stay in ctx (pair_keys_sorted).
+void broad_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_t shard_count,
+                    uint64_t& n_pairs, int& key_bits, float& ms)
+{
+    validate_pipeline_cfg(cfg);
+    DevScene& s = c.scene;
+    const uint64_t k = s.nv + s.ne + s.nf;
+    cudaEvent_t e0 = c.events.get(EventPool::kStep), e1 = c.events.get(EventPool::kStep + 1);
+    CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+    float *bmin, *bmax;
+    uint4* vids;
+    build_resident_boxes(c, cfg, bmin, bmax, vids);
+    n_pairs = 0;
+    key_bits = ceil_log2(std::max<uint64_t>(k, 2));
+    if (k >= 2) {
+        BroadIn bi;
+        bi.bmin = bmin;
+        bi.bmax = bmax;
+        bi.vids = vids;
+        bi.k = k;
+        bi.method = CCDK_BROAD_STQ;
+        bi.shard_rank = shard_rank;
+        bi.shard_count = shard_count;
+        BroadOut bo;
+        broad_phase(c, bi, bo);
+        n_pairs = bo.n_pairs;
+        key_bits = c.last_nb;
+    }
+    c.last_n_pairs = n_pairs;
+    CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
+    CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+}
+
+// Second half: classify + narrow phase on a slice of canonical keys supplied
+// by the caller (device memory), sorted here into canonical order.
+void ccd_keys_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, const uint64_t* keys, uint64_t n,
+                       int key_bits, ccdk_report& rep)
+{
+    validate_pipeline_cfg(cfg);
+    DevScene& s = c.scene;
+    const uint64_t k = s.nv + s.ne + s.nf;
+    if (key_bits != ceil_log2(std::max<uint64_t>(k, 2)))
+        throw Error(CCDK_CONFIG, "ccdk_ccd_keys_resident: key width does not match the resident scene");
+    std::memset(&rep, 0, sizeof rep);
+    rep.toi = INFINITY;
+    rep.batch_count = 1;
+    cudaEvent_t e0 = c.events.get(EventPool::kStep + 2), e1 = c.events.get(EventPool::kStep + 3);
+    CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+    c.last_nb = key_bits;
+    uint64_t* sorted = grow<uint64_t>(c.pair_keys_sorted, std::max<uint64_t>(n, 1));
+    if (n) {
+        cub_call(c, [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, keys, sorted, static_cast<int64_t>(n), 0,
+                                                  2 * key_bits, c.stream);
+        });
+    }
+    const uint64_t cap_pairs = ~0ull;
+    BatchRun run { c, cfg, s, k, cap_pairs };
+    run.process_keys(sorted, n);
+    c.last_keys_all = true;
+    c.last_pairs_general = false;
+    c.last_n_pairs = run.candidates;
+    c.last_query_count = run.queries;
+    const double toi = __builtin_bit_cast(double, static_cast<uint64_t>(run.toi_bits));
+    double* dtoi = grow<double>(c.last_toi, 1);
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(dtoi, &toi, 8, cudaMemcpyHostToDevice, c.stream));
+    CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
+    CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms_total = 0;
+    CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms_total, e0, e1));
+    rep.toi = toi;
+    rep.tolerance_hit = run.tol ? 1 : 0;
+    rep.zero_toi_diagnostic = run.zd ? 1 : 0;
+    rep.candidate_count = run.candidates;
+    rep.query_count = run.queries;
+    rep.batch_count = std::max<uint64_t>(1, run.narrow_batches);
+    rep.vf_count = run.vf;
+    rep.total_splits = run.total_splits;
+    rep.peak_queue = run.peak_queue;
+    rep.evaluations = run.evaluations;
+    rep.split_actions = run.split_actions;
+    rep.generations = run.generations;
+    rep.ms_classify = run.ms_classify;
+    rep.ms_narrow = run.ms_narrow;
+    rep.ms_total = ms_total;
+    rep.kernel_launches = run.launches;
     rep.t_socd = run.ms_classify * 1e-3;
     rep.t_np = run.ms_narrow * 1e-3;
 }
@@ -1193,6 +1312,48 @@ int ccdk_query_min_separations(ccdk_ctx* ctx, const uint8_t* kind, const double*
         launch_min_seps(c, dk, dp, n, *cfg, dout);
         d2h(c, out, dout, 8 * n);
         sync(c);
+    });
+}
+
+int ccdk_broad_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shard_rank,
+                        uint32_t shard_count, uint64_t* n_pairs, int* key_bits, float* device_ms)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (!ctx->scene.valid)
+            throw Error(CCDK_CONFIG, "ccdk_broad_resident: no scene uploaded");
+        if (shard_count < 1 || shard_rank >= shard_count)
+            throw Error(CCDK_CONFIG, "ccdk_broad_resident: bad shard");
+        float ms = 0;
+        broad_resident(*ctx, *cfg, shard_rank, shard_count, *n_pairs, *key_bits, ms);
+        if (device_ms)
+            *device_ms = ms;
+    });
+}
+
+int ccdk_copy_keys_device(ccdk_ctx* ctx, void* dst_dev)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        if (c.last_n_pairs)
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(dst_dev, c.pair_keys_sorted.p, c.last_n_pairs * 8,
+                                            cudaMemcpyDeviceToDevice, c.stream));
+        sync(c);
+    });
+}
+
+int ccdk_ccd_keys_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, const uint64_t* dev_keys,
+                           uint64_t n, int key_bits, ccdk_report* report)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (!ctx->scene.valid)
+            throw Error(CCDK_CONFIG, "ccdk_ccd_keys_resident: no scene uploaded");
+        ccd_keys_resident(*ctx, *cfg, dev_keys, n, key_bits, *report);
     });
 }
 

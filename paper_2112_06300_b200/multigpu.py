@@ -10,6 +10,15 @@ candidate set).  Candidate sets are disjoint by construction (a pair is
 emitted by its lower sorted position), so the data path needs no collective;
 the only exchange is the 8-byte allreduce(min) of the ToI, run on the device
 buffer the step wrote (NCCL over NVLink on GPUs, gloo in the CPU tests).
+
+Narrow-phase load balance: equal sweep work does not mean
+equal candidate counts, so RebalancedCcd splits the step at the candidate
+list: after the sweep, ranks all-gather their counts (N integers) and move
+pair keys with ONE all_to_all so that rank r narrow-phases the r-th equal
+slice of the rank-ordered concatenation of all candidates.  Every rank holds
+the replicated scene, so an 8-byte key is all a rank needs to gather the
+query's coordinates; per-query results are partition-independent
+(narrowphase.hpp:93-96), so the ToI is unchanged.
 """
 from __future__ import annotations
 
@@ -85,3 +94,77 @@ class ShardedCcd:
 
     def global_toi(self, rep) -> float:
         return float(self.toi.item()) if self.world > 1 else rep.toi.toi
+
+
+def balanced_ranges(counts, world: int):
+    """Rank r's slice [lo_r, hi_r) of the rank-ordered concatenation of all
+    ranks' candidates (equal counts up to one)."""
+    total = int(sum(int(c) for c in counts))
+    return [(total * r // world, total * (r + 1) // world) for r in range(world)]
+
+
+def exchange_splits(counts, rank: int, world: int):
+    """all_to_all split sizes that move this rank's candidates (global range
+    [off_rank, off_rank + counts[rank])) to the balanced owners."""
+    counts = [int(c) for c in counts]
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    rng = balanced_ranges(counts, world)
+
+    def overlap(a0, a1, b0, b1):
+        return max(0, min(a1, b1) - max(a0, b0))
+
+    send = [int(overlap(offs[rank], offs[rank + 1], lo, hi)) for lo, hi in rng]
+    lo, hi = rng[rank]
+    recv = [int(overlap(offs[s], offs[s + 1], lo, hi)) for s in range(world)]
+    return send, recv
+
+
+def rebalance_keys(keys, counts, rank: int, world: int, group=None):
+    """Move pair keys (a 1-D int64 tensor holding this rank's counts[rank]
+    keys, any device) so each rank ends with its balanced slice; one
+    all_to_all_single (NCCL on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    send, recv = exchange_splits(counts, rank, world)
+    out = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
+    dist.all_to_all_single(out, keys[:sum(send)].contiguous(), output_split_sizes=recv,
+                           input_split_sizes=send, group=group)
+    return out
+
+
+class RebalancedCcd:
+    """The multi-GPU CCD step with the narrow phase balanced by candidate
+    count: sweep shard -> all_gather(counts) -> all_to_all(keys) -> classify +
+    narrow on the balanced slice -> allreduce(min) of the ToI."""
+
+    def __init__(self, resident, rank: int, world: int, group=None):
+        import torch
+        self.resident = resident
+        self.rank = rank
+        self.world = world
+        self.group = group
+        self.dev = f"cuda:{resident.ctx.device}"
+        self.toi = torch.full((1,), float("inf"), dtype=torch.float64, device=self.dev)
+        self.keys = torch.empty(0, dtype=torch.int64, device=self.dev)
+
+    def step(self, cfg):
+        import torch
+        import torch.distributed as dist
+        n, nb, broad_ms = self.resident.broad(cfg, self.rank, self.world)
+        cnt = torch.tensor([n], dtype=torch.int64, device=self.dev)
+        counts = [torch.zeros(1, dtype=torch.int64, device=self.dev) for _ in range(self.world)]
+        dist.all_gather(counts, cnt, group=self.group)
+        counts = [int(c.item()) for c in counts]
+        if self.keys.numel() < max(n, 1):
+            self.keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
+        self.resident.copy_keys(self.keys.data_ptr())
+        mine = rebalance_keys(self.keys, counts, self.rank, self.world, self.group)
+        rep = self.resident.narrow_keys(cfg, mine.data_ptr(), mine.numel(), nb)
+        self.resident.copy_toi_to(self.toi.data_ptr())
+        allreduce_min_toi(self.toi, self.group)
+        rep.shard_counts = counts
+        rep.device["ms_broad"] = broad_ms  # box build + sweep shard + pair sort
+        return rep
+
+    def global_toi(self, rep) -> float:
+        return float(self.toi.item())

@@ -61,6 +61,11 @@ _SIGS = {
     "ccdk_narrow_phase_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                            C.POINTER(abi.NarrowCfg), C.c_uint64, C.c_void_p, C.c_void_p,
                                            C.POINTER(abi.NarrowStats)]),
+    "ccdk_broad_resident": (C.c_int, [C.c_void_p, C.POINTER(abi.PipelineCfg), C.c_uint32, C.c_uint32,
+                                      C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_float)]),
+    "ccdk_copy_keys_device": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ccdk_ccd_keys_resident": (C.c_int, [C.c_void_p, C.POINTER(abi.PipelineCfg), C.c_void_p, C.c_uint64,
+                                         C.c_int, C.POINTER(abi.Report)]),
     "ccdk_inclusion_boxes": (C.c_int, [C.c_void_p, P_U8, P_F64, P_F64, C.c_uint64, P_F64]),
     "ccdk_process_intervals": (C.c_int, [C.c_void_p, P_U8, P_F64, P_F64, P_U16, P_F64, P_F64,
                                          C.c_uint64, C.POINTER(abi.NarrowCfg), P_U8, P_F64, P_U8,

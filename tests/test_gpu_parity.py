@@ -463,3 +463,45 @@ def test_c5_partition_independence(ctx):
     np.testing.assert_array_equal(big.flags[idx], small.flags)
     assert big.global_toi == big.toi.min()
     assert int((big.flags & abi.FLAG_TOLERANCE_HIT).astype(bool).sum()) >= 1  # a budget bomb is in the batch
+
+
+# ------------------------------------------------- multi-GPU rebalance (1 GPU)
+
+def test_rebalanced_shards_match_full_step(ctx):
+    """The rebalanced multi-GPU step, simulated with two shards on one device:
+    the shards' sweep keys union to the full candidate set; narrow-phasing
+    equal-count slices of their concatenation (ccdk_ccd_keys_resident)
+    reproduces the full step's global ToI and every query's ToI / flags."""
+    import torch
+    from paper_2112_06300_b200.multigpu import balanced_ranges
+    s = scenes.make_cloth_scene(40, 40, 0.02, 1.0, 4)
+    cfg = PipelineConfig(inflation=0.01)
+    rs = ck.ResidentScene(s, ctx)
+    full = rs.step(cfg)
+    full_keys = None
+    shard_keys = []
+    for r in range(2):
+        n, nb, _ = rs.broad(cfg, r, 2)
+        t = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+        rs.copy_keys(t.data_ptr())
+        shard_keys.append(t[:n].cpu().numpy().view(np.uint64))
+    n_all, nb, _ = rs.broad(cfg, 0, 1)
+    t = torch.empty(n_all, dtype=torch.int64, device="cuda")
+    rs.copy_keys(t.data_ptr())
+    full_keys = t.cpu().numpy().view(np.uint64)
+    concat = np.concatenate(shard_keys)
+    assert np.array_equal(np.sort(concat), full_keys)
+    assert len(full_keys) == full.candidate_count
+    # full-step per-query results, indexed by canonical key
+    rs.step(cfg)
+    ftoi, ffl = rs.query_results(full.query_count)
+    toi = np.inf
+    for lo, hi in balanced_ranges([len(k) for k in shard_keys], 2):
+        sl = torch.from_numpy(concat[lo:hi].view(np.int64).copy()).cuda()
+        rep = rs.narrow_keys(cfg, sl.data_ptr(), hi - lo, nb)
+        toi = min(toi, rep.toi.toi)
+        qt, qf = rs.query_results(rep.query_count)
+        pos = np.searchsorted(full_keys, np.sort(concat[lo:hi]))
+        assert_bits(qt, ftoi[pos])
+        np.testing.assert_array_equal(qf, ffl[pos])
+    assert toi == full.toi.toi

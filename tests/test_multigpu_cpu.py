@@ -91,3 +91,62 @@ def test_shard_bounds_partition(count):
     total = int(run_len[10:990].sum())
     for lo, hi in bounds:  # every shard's work is within one row of the ideal share
         assert int(run_len[lo:hi].sum()) <= total / count + int(run_len.max())
+
+
+def _rebalance_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_06300_b200.multigpu import balanced_ranges, rebalance_keys
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    counts = [37, 5] if world == 2 else [1] * world
+    rng = np.random.default_rng(100 + rank)
+    keys = torch.from_numpy(rng.integers(0, 1 << 40, counts[rank], dtype=np.int64))
+    mine = rebalance_keys(keys, counts, rank, world)
+    # what every rank holds, gathered for the check
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([mine.numel()], dtype=torch.int64))
+    mx = max(int(x.item()) for x in sizes)
+    buf = torch.zeros(mx, dtype=torch.int64)
+    buf[:mine.numel()] = mine
+    got = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(got, buf)
+    src = [torch.zeros(max(counts), dtype=torch.int64) for _ in range(world)]
+    pad = torch.zeros(max(counts), dtype=torch.int64)
+    pad[:keys.numel()] = keys
+    dist.all_gather(src, pad)
+    if rank == 0:
+        concat = np.concatenate([s[:c].numpy() for s, c in zip(src, counts)])
+        held = [g[:int(n.item())].numpy() for g, n in zip(got, sizes)]
+        rngs = balanced_ranges(counts, world)
+        ok = all(np.array_equal(h, concat[lo:hi]) for h, (lo, hi) in zip(held, rngs))
+        ok = ok and max(len(h) for h in held) - min(len(h) for h in held) <= 1
+        with open(result_path, "w") as f:
+            f.write("ok" if ok else "bad")
+    dist.destroy_process_group()
+
+
+def test_rebalance_keys_gloo_world2(tmp_path):
+    """after the sweep, one all_to_all moves pair keys so each
+    rank holds an equal slice (within one) of the rank-ordered concatenation."""
+    import torch.multiprocessing as mp
+    out = tmp_path / "res.txt"
+    mp.start_processes(_rebalance_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True,
+                       start_method="spawn")
+    assert out.read_text() == "ok"
+
+
+def test_exchange_splits_host():
+    from paper_2112_06300_b200.multigpu import balanced_ranges, exchange_splits
+    counts = [10, 3, 7, 0]
+    rng = balanced_ranges(counts, 4)
+    assert [hi - lo for lo, hi in rng] == [5, 5, 5, 5]
+    sends = [exchange_splits(counts, r, 4)[0] for r in range(4)]
+    recvs = [exchange_splits(counts, r, 4)[1] for r in range(4)]
+    for r in range(4):
+        assert sum(sends[r]) == counts[r]
+        assert sum(recvs[r]) == rng[r][1] - rng[r][0]
+        for s in range(4):
+            assert sends[s][r] == recvs[r][s]
