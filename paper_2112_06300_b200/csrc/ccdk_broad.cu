@@ -430,8 +430,14 @@ __global__ void __launch_bounds__(kTB) k_sweep_tile(SweepArgs a)
 // (keep_pair, which needs the other box's vertex ids) runs on 32 of them at a
 // time with every lane busy, instead of a dependent load per stride.  Rows
 // whose window exceeds kCap spill the rest to k_sweep_heavy segments.
-constexpr int kRowsPerWarp = 8;
-constexpr int kRowsTB = 256;
+#ifndef CCDK_SWEEP_RPW
+#define CCDK_SWEEP_RPW 8
+#endif
+#ifndef CCDK_SWEEP_TB
+#define CCDK_SWEEP_TB 1024
+#endif
+constexpr int kRowsPerWarp = CCDK_SWEEP_RPW;
+constexpr int kRowsTB = CCDK_SWEEP_TB;
 #ifndef CCDK_SWEEP_UNROLL
 #define CCDK_SWEEP_UNROLL 4
 #endif

@@ -505,3 +505,29 @@ def test_rebalanced_shards_match_full_step(ctx):
         assert_bits(qt, ftoi[pos])
         np.testing.assert_array_equal(qf, ffl[pos])
     assert toi == full.toi.toi
+
+
+def test_c4_full_size_bit_exact(ctx):
+    """BASELINE config 4 at full size (1,005,334 primitives) against the
+    unmodified reference on all host cores: identical candidate count, and
+    every query's ToI / flags bit-identical (queries in canonical order)."""
+    import os
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    s = scenes.config_scene("C4")
+    cfg = PipelineConfig(inflation=0.01)
+    rs = ck.ResidentScene(s, ctx)
+    rep = rs.step(cfg)
+    got_pairs = rs.candidates(rep.candidate_count)
+    toi, flags = rs.query_results(rep.query_count)
+    r = oracle.ref(os.cpu_count() or 1)
+    cref = PipelineConfig(inflation=0.01, broad_method=ck.BROAD_SAP, threads=os.cpu_count() or 1)
+    exp, pairs = r.ccd(s, cref.to_c())
+    assert rep.candidate_count == exp.candidate_count
+    np.testing.assert_array_equal(got_pairs, pairs)
+    assert rep.toi.toi == exp.toi
+    kind, pts, _, _ = r.classify(pairs, s)
+    etoi, efl, st = r.narrow_phase(kind, pts, NarrowConfig().to_c())
+    assert_bits(toi, etoi)
+    np.testing.assert_array_equal(flags, efl)
