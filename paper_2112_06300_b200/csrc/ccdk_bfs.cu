@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     const unsigned long long W = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long b = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x >> 5) + wib;
     unsigned evals = 0, split_actions = 0, dropped = 0;
+#ifdef CCDK_STATS
+    unsigned st_pairs = 0, st_single = 0;
+#endif
     if (b >= nbatch)
         return; // warp-uniform; no __syncthreads in this kernel
 
@@ -406,6 +409,10 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                     alive[ch] = !(clo[ch][0] >= t_star || clo[ch][0] >= a.cfg.t_max)
                         && !(vf && __dadd_rn(clo[ch][1], clo[ch][2]) > 1.0);
                 }
+#ifdef CCDK_STATS
+                st_pairs += (alive[0] || alive[1]);
+                st_single += (alive[0] != alive[1]);
+#endif
                 if (alive[0] || alive[1]) {
                     // per-query separation (Relative min-separation mode only)
                     const double sep = a.sep ? a.sep[q] : a.sep_default;
@@ -478,6 +485,10 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);
     warp_add(&sc->dropped, dropped);
+#ifdef CCDK_STATS
+    warp_add(&sc->vf_count, st_pairs);       // diagnostics only: pairs with a live child
+    warp_add(&sc->next_n, st_single);        // diagnostics only: pairs with exactly one live child
+#endif
 }
 
 // Generation end: refresh snapshots of queries whose ToI dropped, then (last
@@ -985,6 +996,10 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
     CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
     c.narrow_launches += 3 + (kGenSplit ? 4 : 2) * host_sc->gen;
+#ifdef CCDK_STATS
+    fprintf(stderr, "[ccdk stats] pairs with a live child %llu, with exactly one %llu\n", host_sc->vf_count,
+            host_sc->next_n);
+#endif
     if (debug_enabled())
         fprintf(stderr, "[ccdk narrow] n=%llu gen=%llu peak=%llu evals=%llu splits=%llu phys=%llu sem=%llu\n",
                 (unsigned long long)n, host_sc->gen, host_sc->peak, host_sc->evaluations,

@@ -145,10 +145,79 @@ __global__ void k_sort_keys(const float* bmin, unsigned long long k, const int* 
     vals[s] = static_cast<uint32_t>(s);
 }
 
+// ---- quantised 2-axis filter boxes for the sweep.
+// The sweep's pair test on the two non-sweep axes runs first on 15-bit
+// quantised boxes (8 bytes instead of 16): q = floor((x - lo) * s) for a min,
+// ceil(...) for a max, clamped to [0, 32767], with the same fp32 operations
+// for every box.  That map is monotone non-decreasing, so min_j <= max_i
+// implies q(min_j) <= q(max_i): the quantised test passes every exactly
+// overlapping pair (a superset), and each pass is re-tested on the exact
+// fp32 box before keep_pair.  The sweep is L1-bandwidth bound, so halving
+// the bytes per test is what matters.
+__device__ __forceinline__ unsigned f2ord(float f)
+{
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned o)
+{
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+// qb[0..2] = ordered min of bmin per axis, qb[3..5] = ordered max of bmax
+// (qb pre-set to 0xffffffff / 0).
+__global__ void k_quant_bounds(const float* bmin, const float* bmax, unsigned long long k, unsigned* qb)
+{
+    unsigned lo[3] = { 0xffffffffu, 0xffffffffu, 0xffffffffu }, hi[3] = { 0, 0, 0 };
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < k;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = min(lo[a], f2ord(bmin[a * k + i]));
+            hi[a] = max(hi[a], f2ord(bmax[a * k + i]));
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&qb[a], lo[a]);
+            atomicMax(&qb[3 + a], hi[a]);
+        }
+    }
+}
+
+struct QuantAxis {
+    float lo, s;
+};
+__device__ __forceinline__ QuantAxis quant_axis(const unsigned* qb, int a)
+{
+    const float lo = ord2f(qb[a]), hi = ord2f(qb[3 + a]);
+    const float ext = __fsub_rn(hi, lo);
+    QuantAxis q { lo, 0.0f };
+    if (isfinite(lo) && isfinite(hi) && isfinite(ext) && ext > 0.0f)
+        q.s = __fdiv_rn(32767.0f, ext);
+    return q; // s == 0: every box quantises to 0 (the filter passes all)
+}
+__device__ __forceinline__ unsigned quant_dn(QuantAxis q, float x)
+{
+    const float v = floorf(__fmul_rn(__fsub_rn(x, q.lo), q.s));
+    return v <= 0.0f ? 0u : v >= 32767.0f ? 32767u : static_cast<unsigned>(v);
+}
+__device__ __forceinline__ unsigned quant_up(QuantAxis q, float x)
+{
+    const float v = ceilf(__fmul_rn(__fsub_rn(x, q.lo), q.s));
+    return v <= 0.0f ? 0u : v >= 32767.0f ? 32767u : static_cast<unsigned>(v);
+}
+
 __global__ void k_permute(const float* bmin, const float* bmax, const uint4* vids,
                           const uint32_t* raw, unsigned long long k, const int* axis,
                           const uint32_t* order, float* smin_a, float* smax_a, float4* sbox,
-                          uint4* svid, uint32_t* sraw)
+                          uint4* svid, uint32_t* sraw, const unsigned* qb, uint2* sq)
 {
     const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (p >= k)
@@ -157,7 +226,10 @@ __global__ void k_permute(const float* bmin, const float* bmax, const uint4* vid
     const unsigned long long s = order[p];
     smin_a[p] = bmin[a * k + s];
     smax_a[p] = bmax[a * k + s];
-    sbox[p] = make_float4(bmin[a1 * k + s], bmax[a1 * k + s], bmin[a2 * k + s], bmax[a2 * k + s]);
+    const float4 b = make_float4(bmin[a1 * k + s], bmax[a1 * k + s], bmin[a2 * k + s], bmax[a2 * k + s]);
+    sbox[p] = b;
+    const QuantAxis q1 = quant_axis(qb, a1), q2 = quant_axis(qb, a2);
+    sq[p] = make_uint2(quant_dn(q1, b.x) | (quant_dn(q2, b.z) << 16), quant_up(q1, b.y) | (quant_up(q2, b.w) << 16));
     svid[p] = vids[s];
     if (sraw)
         sraw[p] = raw ? raw[s] : static_cast<uint32_t>(s);
@@ -279,6 +351,7 @@ struct SweepArgs {
     const float* smin_a;
     const float* smax_a;
     const float4* sbox;
+    const uint2* sq;           // quantised filter boxes (lo = qmin_b | qmin_c << 16, hi = qmax_b | qmax_c << 16)
     const uint4* svid;
     const uint32_t* sraw;      // bf mode only
     const uint32_t* run_end;
@@ -444,25 +517,27 @@ constexpr int kRowsTB = CCDK_SWEEP_TB;
 constexpr int kUnroll = CCDK_SWEEP_UNROLL;
 constexpr int kHitBuf = 32 * kUnroll + 32; // < 32 left over + kUnroll strides
 
-__device__ __forceinline__ void filter_hits(const SweepArgs& a, unsigned long long p, uint4 mv,
+__device__ __forceinline__ void filter_hits(const SweepArgs& a, unsigned long long p, float4 mb, uint4 mv,
                                             const unsigned* hits, unsigned cnt, unsigned lane)
 {
-    const bool h = lane < cnt;
+    bool h = lane < cnt;
     const unsigned long long q = p + (h ? hits[lane] : 0u);
+    // the quantised pass is a superset: the exact fp32 test decides
+    h = h && box_hit(mb, a.sbox[q]);
     const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
     emit(a, h && keep_pair(mv, ov) && bf_ok(a, p, q), mv.w, ov.w);
 }
 
 // Run the filter on every full chunk of 32 (all of them when `all`) and
 // move the remainder to the front of the list.
-__device__ __forceinline__ void drain_hits(const SweepArgs& a, unsigned long long p, uint4 mv,
+__device__ __forceinline__ void drain_hits(const SweepArgs& a, unsigned long long p, float4 mb, uint4 mv,
                                            unsigned* hits, unsigned& nh, unsigned lane, bool all)
 {
     __syncwarp();
     unsigned base = 0;
     while (nh - base >= 32 || (all && nh > base)) {
         const unsigned cnt = min(nh - base, 32u);
-        filter_hits(a, p, mv, hits + base, cnt, lane);
+        filter_hits(a, p, mb, mv, hits + base, cnt, lane);
         base += cnt;
     }
     const unsigned rem = nh - base; // < 32
@@ -482,25 +557,38 @@ __device__ __forceinline__ void push_hit(unsigned* hits, unsigned& nh, bool h, u
     nh += __popc(m);
 }
 
+// Quantised 2-axis overlap (superset of the exact test): per 16-bit lane,
+// (0x8000 + a) - b keeps bit 15 iff a >= b (15-bit values: no borrow across
+// lanes), so one subtract checks both axes of one inequality.
+constexpr unsigned kGuard = 0x80008000u;
+__device__ __forceinline__ bool qhit(unsigned m_hi_g, unsigned m_lo, uint2 o)
+{
+    const unsigned x1 = m_hi_g - o.x;          // o.qmin <= m.qmax
+    const unsigned x2 = (o.y | kGuard) - m_lo; // m.qmin <= o.qmax
+    return (x1 & x2 & kGuard) == kGuard;
+}
+
 // Row p against boxes [jb, je) of its window (warp-cooperative).
 __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long long p, unsigned long long jb,
                                              unsigned long long je, unsigned* hits, unsigned lane)
 {
     const float4 mb = a.sbox[p];
     const uint4 mv = a.svid[p];
+    const uint2 mq = a.sq[p];
+    const unsigned m_hi_g = mq.y | kGuard, m_lo = mq.x;
     unsigned nh = 0;             // warp-uniform
     unsigned long long j0 = jb;  // warp-uniform stride base
     // kUnroll full strides per iteration: all loads in flight before the tests
     for (; j0 + 32 * kUnroll <= je; j0 += 32 * kUnroll) {
         const unsigned long long j = j0 + lane;
-        float4 o[kUnroll];
+        uint2 o[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-            o[u] = __ldg(&a.sbox[j + 32 * u]);
+            o[u] = __ldg(&a.sq[j + 32 * u]);
         bool h[kUnroll], any = false;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            h[u] = box_hit(mb, o[u]);
+            h[u] = qhit(m_hi_g, m_lo, o[u]);
             any = any || h[u];
         }
         if (__any_sync(0xffffffffu, any)) {
@@ -508,18 +596,18 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
             for (int u = 0; u < kUnroll; ++u)
                 push_hit(hits, nh, h[u], static_cast<unsigned>(j + 32 * u - p), lane);
             if (nh >= 32)
-                drain_hits(a, p, mv, hits, nh, lane, false);
+                drain_hits(a, p, mb, mv, hits, nh, lane, false);
         }
     }
     // ragged tail (< 32 kUnroll boxes): lanes past the window end are idle
     for (; j0 < je; j0 += 32) {
         const unsigned long long j = j0 + lane;
         const bool valid = j < je;
-        const bool h = valid && box_hit(mb, __ldg(&a.sbox[valid ? j : p]));
+        const bool h = valid && qhit(m_hi_g, m_lo, __ldg(&a.sq[valid ? j : p]));
         push_hit(hits, nh, h, static_cast<unsigned>(j - p), lane);
     }
     if (nh)
-        drain_hits(a, p, mv, hits, nh, lane, true);
+        drain_hits(a, p, mb, mv, hits, nh, lane, true);
 }
 
 __global__ void __launch_bounds__(kRowsTB) k_sweep_rows(SweepArgs a)
@@ -645,8 +733,13 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     uint4* svid = grow<uint4>(c.svid, k);
     const bool bf = in.method == CCDK_BROAD_BF;
     uint32_t* sraw = bf ? grow<uint32_t>(c.raw, 2 * k) + k : nullptr;
+    unsigned* qb = static_cast<unsigned*>(c.qbounds.ensure(8 * sizeof(unsigned)));
+    CCDK_CUDA_CHECK(cudaMemsetAsync(qb, 0xff, 3 * sizeof(unsigned), s));
+    CCDK_CUDA_CHECK(cudaMemsetAsync(qb + 3, 0, 3 * sizeof(unsigned), s));
+    k_quant_bounds<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, qb);
+    uint2* sq = grow<uint2>(c.squant, k);
     k_permute<<<grid_for(k, 256), 256, 0, s>>>(in.bmin, in.bmax, in.vids, in.raw, k, d_axis, order,
-                                               smin_a, smax_a, sbox, svid, sraw);
+                                               smin_a, smax_a, sbox, svid, sraw, qb, sq);
     CCDK_LAUNCH_CHECK();
     CCDK_CUDA_CHECK(cudaEventRecord(ev[1], s));
 
@@ -746,6 +839,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         sa.smin_a = smin_a;
         sa.smax_a = smax_a;
         sa.sbox = sbox;
+        sa.sq = sq;
         sa.svid = svid;
         sa.sraw = sraw;
         sa.run_end = run_end;

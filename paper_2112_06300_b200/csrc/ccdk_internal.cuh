@@ -318,6 +318,8 @@ struct Ctx {
     DevBuf own_kind, own_index;        // owner of each slot (general mode)
     DevBuf sort_keys_in, sort_keys_out, sort_vals_in, sort_vals_out;
     DevBuf smin_a, smax_a, sbox, svid; // sorted SoA
+    DevBuf squant;                     // sorted quantised filter boxes (uint2)
+    DevBuf qbounds;                    // quantisation bounds (ordered u32 min[3], max[3])
     DevBuf run_end, seg_off, segs, prefix;
     DevBuf pair_keys, pair_keys_sorted;
     DevBuf rounds;
