@@ -578,13 +578,15 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
     const unsigned m_hi_g = mq.y | kGuard, m_lo = mq.x;
     unsigned nh = 0;             // warp-uniform
     unsigned long long j0 = jb;  // warp-uniform stride base
-    // kUnroll full strides per iteration: all loads in flight before the tests
-    for (; j0 + 32 * kUnroll <= je; j0 += 32 * kUnroll) {
-        const unsigned long long j = j0 + lane;
+    // kUnroll full strides per iteration: all loads in flight before the
+    // tests; one advancing pointer, so the loads use immediate offsets
+    const uint2* qp = a.sq + j0 + lane;
+    unsigned off = static_cast<unsigned>(j0 - p) + lane; // this lane's box offset from p
+    for (; j0 + 32 * kUnroll <= je; j0 += 32 * kUnroll, qp += 32 * kUnroll, off += 32 * kUnroll) {
         uint2 o[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-            o[u] = __ldg(&a.sq[j + 32 * u]);
+            o[u] = __ldg(qp + 32 * u);
         bool h[kUnroll], any = false;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -594,7 +596,7 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
         if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
-                push_hit(hits, nh, h[u], static_cast<unsigned>(j + 32 * u - p), lane);
+                push_hit(hits, nh, h[u], off + 32 * u, lane);
             if (nh >= 32)
                 drain_hits(a, p, mb, mv, hits, nh, lane, false);
         }
