@@ -9,15 +9,16 @@
 //                    the STQ queue holds (p, j) in round j-p-1 for exactly the
 //                    j in (p, U[p]), so StqStats follow from run lengths and a
 //                    prefix sum partitions equal pair-test work per shard
-//   K5 sweep         CTA = 128 consecutive left rows; the union of their
-//                    j-windows is staged through shared memory in 256-box
-//                    tiles and read as broadcasts; a warp skips tiles none of
-//                    its rows need; hits (rare) run keep_pair (type + shared
-//                    vertex, broadphase.cpp:12-20) and append u64 pair keys
-//                    with one warp-aggregated atomic per ballot.  Rows whose
-//                    window exceeds CAP spill the remainder as SEG-sized
-//                    segments handled warp-per-segment (load balance for the
-//                    static floor / container walls whose window is ~k).
+//   K5 sweep         one warp per left row at a time, lanes over the row's
+//                    j-window with coalesced loads of 15-bit quantised
+//                    filter boxes (8 B, conservative); filter passes are
+//                    compacted per warp and re-tested exactly (fp32) plus
+//                    keep_pair (type + shared vertex, broadphase.cpp:12-20)
+//                    32 at a time; survivors append u64 pair keys with one
+//                    warp-aggregated atomic per ballot.  Windows beyond kCap
+//                    spill the rest as kSeg-sized segments walked by the
+//                    same code (load balance for static floors / walls
+//                    whose window is ~k).
 //   K6 pair sort     CUB radix sort of (lo_rank << nb | hi_rank) over 2*nb bits
 //                    = canonical CandidatePair order (finalize, 37-41).
 #include <math_constants.h>
@@ -31,9 +32,7 @@ namespace ccdk {
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
-constexpr int kTB = 128;        // left rows per sweep CTA
-constexpr int kTile = 512;      // staged boxes per tile (8 KiB of float4)
-constexpr uint32_t kCap = 4096; // per-row window handled by the tile kernel
+constexpr uint32_t kCap = 4096; // per-row window handled by k_sweep_rows; the rest goes to k_sweep_heavy
 constexpr uint32_t kSeg = 2048; // heavy-row segment length
 constexpr int kRedBlocks = 256;
 constexpr int kRedThreads = 256;
@@ -418,80 +417,6 @@ __device__ __forceinline__ bool bf_ok(const SweepArgs& a, unsigned long long p, 
     return r >= a.bf_lo && r < a.bf_hi && a.smin_a[p] <= a.smax_a[j];
 }
 
-__global__ void __launch_bounds__(kTB) k_sweep_tile(SweepArgs a)
-{
-    __shared__ float4 s_box[kTile + 4];
-    __shared__ unsigned s_span;
-    const unsigned long long B = a.range[0], E = a.range[1];
-    const unsigned long long base = a.row0 + static_cast<unsigned long long>(blockIdx.x) * kTB;
-    if (base >= E || base + kTB <= B)
-        return;
-    const unsigned long long p = base + threadIdx.x;
-    const bool row = p >= B && p < E;
-    float4 mb = make_float4(0, 0, 0, 0);
-    uint4 mv = make_uint4(0, 0, 0, 0);
-    unsigned long long je = p + 1;
-    if (row) {
-        mb = a.sbox[p];
-        mv = a.svid[p];
-        je = min(static_cast<unsigned long long>(a.run_end[p]), p + 1 + kCap);
-    }
-    if (threadIdx.x == 0)
-        s_span = 0;
-    __syncthreads();
-    // window offsets relative to `base` fit in 32 bits (< kTB + kCap + 1)
-    const unsigned jb_off = static_cast<unsigned>(p + 1 - base);
-    const unsigned je_off = static_cast<unsigned>(je - base);
-    if (row && je_off > jb_off)
-        atomicMax(&s_span, je_off);
-    const unsigned w_lo = __reduce_min_sync(0xffffffffu, (row && je_off > jb_off) ? jb_off : 0xffffffffu);
-    const unsigned w_hi = __reduce_max_sync(0xffffffffu, (row && je_off > jb_off) ? je_off : 0u);
-    __syncthreads();
-    const unsigned span = s_span;
-    // per-lane window [jb_off, je_off) as (start, length): one unsigned
-    // compare tests both ends
-    const unsigned len = (row && je_off > jb_off) ? je_off - jb_off : 0u;
-    for (unsigned c0 = 1; c0 < span; c0 += kTile) {
-        const unsigned n = min(static_cast<unsigned>(kTile), span - c0);
-        for (unsigned t = threadIdx.x; t < n; t += kTB)
-            s_box[t] = a.sbox[base + c0 + t];
-        __syncthreads();
-        const unsigned j0 = max(c0, w_lo), j1 = min(c0 + n, w_hi);
-        const float4* sp = s_box - c0;
-        unsigned j = j0;
-        // 4 boxes per vote: LDS.128 broadcast + 4 compares + 1 range test each
-        for (; j + 4 <= j1; j += 4) {
-            const float4 o0 = sp[j], o1 = sp[j + 1], o2 = sp[j + 2], o3 = sp[j + 3];
-            const bool h0 = (j - jb_off) < len && box_hit(mb, o0);
-            const bool h1 = (j + 1 - jb_off) < len && box_hit(mb, o1);
-            const bool h2 = (j + 2 - jb_off) < len && box_hit(mb, o2);
-            const bool h3 = (j + 3 - jb_off) < len && box_hit(mb, o3);
-            if (__any_sync(0xffffffffu, h0 | h1 | h2 | h3)) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const bool h = u == 0 ? h0 : u == 1 ? h1 : u == 2 ? h2 : h3;
-                    if (__any_sync(0xffffffffu, h)) {
-                        const unsigned long long q = base + j + u;
-                        const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
-                        const bool keep = h && keep_pair(mv, ov) && bf_ok(a, p, q);
-                        emit(a, keep, mv.w, ov.w);
-                    }
-                }
-            }
-        }
-        for (; j < j1; ++j) {
-            const bool h = (j - jb_off) < len && box_hit(mb, sp[j]);
-            if (__any_sync(0xffffffffu, h)) {
-                const unsigned long long q = base + j;
-                const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
-                const bool keep = h && keep_pair(mv, ov) && bf_ok(a, p, q);
-                emit(a, keep, mv.w, ov.w);
-            }
-        }
-        __syncthreads();
-    }
-}
-
 // K5 sweep, row-parallel form: one warp per row at a time, lanes over the
 // row's window [p+1, min(run_end, p+1+kCap)) in 32-box strides with
 // coalesced float4 loads.  A warp walks kRowsPerWarp consecutive rows and a
@@ -857,15 +782,10 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         sa.n_pairs = &ctr->n_pairs;
         sa.segs = segs;
         sa.n_heavy = &ctr->n_heavy;
-#ifndef CCDK_SWEEP_TILE
         if (hi > lo) {
             const uint64_t warps = (hi - lo + kRowsPerWarp - 1) / kRowsPerWarp;
             k_sweep_rows<<<grid_for(warps * 32, kRowsTB), kRowsTB, 0, s>>>(sa);
         }
-#else
-        if (hi > lo)
-            k_sweep_tile<<<grid_for(hi - lo, kTB), kTB, 0, s>>>(sa);
-#endif
         k_sweep_heavy<<<4 * c.num_sms, kRowsTB, 0, s>>>(sa);
         CCDK_LAUNCH_CHECK();
         read_ctr();
