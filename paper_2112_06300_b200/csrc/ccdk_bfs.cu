@@ -233,18 +233,11 @@ struct BatchLoc {
 // Batch b of the concatenated region batch space (regions padded to whole
 // batches so a batch's split dimension is warp-uniform).  Scalar selects, no
 // runtime-indexed arrays (those would live in local memory).
-template <int DSEL>
 __device__ __forceinline__ BatchLoc locate(unsigned long long nb0, unsigned long long nb1,
                                            unsigned long long c0, unsigned long long c1,
                                            unsigned long long c2, unsigned long long b)
 {
     BatchLoc L;
-    if (DSEL != 3) {
-        L.d = DSEL;
-        L.n = DSEL == 0 ? c0 : DSEL == 1 ? c1 : c2;
-        L.i0 = b << 5;
-        return L;
-    }
     if (b < nb0) {
         L.d = 0;
         L.n = c0;
@@ -273,10 +266,6 @@ __device__ __forceinline__ iv::PairOutcome eval_pair(bool vf, const iv::SmemPts&
     return iv::process_pair<D, iv::SmemPts>(vf, P, pb, alive, sep, cfg);
 }
 
-// DSEL = 0, 1, 2: the records of that split dimension only (the three
-// instances run as independent graph nodes, each with the register budget of
-// its own pair evaluation); DSEL = 3: all regions in one launch.
-template <int DSEL>
 __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs a)
 {
     extern __shared__ double gsm[];
@@ -285,9 +274,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
         return;
     const unsigned gen = static_cast<unsigned>(sc->gen);
     const int cb = gen & 1, nb = cb ^ 1;
-    const unsigned long long c0 = (DSEL == 3 || DSEL == 0) ? sc->cur_pairs[0] : 0;
-    const unsigned long long c1 = (DSEL == 3 || DSEL == 1) ? sc->cur_pairs[1] : 0;
-    const unsigned long long c2 = (DSEL == 3 || DSEL == 2) ? sc->cur_pairs[2] : 0;
+    const unsigned long long c0 = sc->cur_pairs[0], c1 = sc->cur_pairs[1], c2 = sc->cur_pairs[2];
     const unsigned long long nb0 = (c0 + 31) >> 5, nb1 = (c1 + 31) >> 5, nb2 = (c2 + 31) >> 5;
     const unsigned long long nbatch = nb0 + nb1 + nb2;
     const unsigned lane = threadIdx.x & 31;
@@ -307,7 +294,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     auto issue = [&](unsigned long long bb, unsigned q, int st) {
         // batch bb's coordinates + record + query scalars, batch bb+W's ids
         if (bb < nbatch) {
-            const BatchLoc L = locate<DSEL>(nb0, nb1, c0, c1, c2, bb);
+            const BatchLoc L = locate(nb0, nb1, c0, c1, c2, bb);
             const unsigned long long i = L.i0 + lane;
             if (i < L.n) {
                 const Region& R = region(a, cb, L.d);
@@ -328,7 +315,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
             }
         }
         if (bb + W < nbatch) {
-            const BatchLoc L = locate<DSEL>(nb0, nb1, c0, c1, c2, bb + W);
+            const BatchLoc L = locate(nb0, nb1, c0, c1, c2, bb + W);
             const unsigned long long i = L.i0 + lane;
             if (i < L.n)
                 cp_async4(qbuf + lane, region(a, cb, L.d).qid + i);
@@ -341,7 +328,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     const unsigned long long req_bound = 2 * (c0 + c1 + c2);
     unsigned q_cur;
     {
-        const BatchLoc L = locate<DSEL>(nb0, nb1, c0, c1, c2, b);
+        const BatchLoc L = locate(nb0, nb1, c0, c1, c2, b);
         const unsigned long long i = L.i0 + lane;
         q_cur = i < L.n ? region(a, cb, L.d).qid[i] : 0u;
     }
@@ -350,7 +337,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
 
     for (; b < nbatch; b += W) {
         cp_async_wait<0>(); // batch b's data and batch b+W's ids (issued one batch ago)
-        const BatchLoc L = locate<DSEL>(nb0, nb1, c0, c1, c2, b);
+        const BatchLoc L = locate(nb0, nb1, c0, c1, c2, b);
         const bool valid = L.i0 + lane < L.n;
         const unsigned q = q_cur;
         const double tlo = meta[32 * kMT + lane];
@@ -419,9 +406,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                     const iv::SmemPts P { stage0 + st * kStageDoubles + lane };
                     iv::PairOutcome o;
                     if (!(qf & iv::kKindExact)) {
-                        if (DSEL != 3)
-                            o = eval_pair<DSEL == 3 ? 0 : DSEL>(vf, P, pb, alive, sep, a.cfg);
-                        else if (D == 0)
+                        if (D == 0)
                             o = eval_pair<0>(vf, P, pb, alive, sep, a.cfg);
                         else if (D == 1)
                             o = eval_pair<1>(vf, P, pb, alive, sep, a.cfg);
@@ -775,34 +760,18 @@ T* grow(DevBuf& b, uint64_t n)
 // Build (or reuse) the generation graph:
 //   k_gen0 -> k_finish -> WHILE(cond) { k_generation -> k_finish }.
 // The condition defaults to 1 at every launch; k_finish clears it.
-#ifndef CCDK_GEN_SPLIT
-#define CCDK_GEN_SPLIT 0 // 1: one k_generation instance per split dimension as parallel graph nodes (measured no faster)
-#endif
-constexpr bool kGenSplit = CCDK_GEN_SPLIT != 0;
-
-void* gen_kernel(int dsel)
-{
-    switch (dsel) {
-    case 0: return reinterpret_cast<void*>(k_generation<0>);
-    case 1: return reinterpret_cast<void*>(k_generation<1>);
-    case 2: return reinterpret_cast<void*>(k_generation<2>);
-    default: return reinterpret_cast<void*>(k_generation<3>);
-    }
-}
-
-void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, const unsigned gen_grid[4], unsigned fin_grid)
+void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_grid, unsigned fin_grid)
 {
     GenGraph& G = c.gen_graph;
     struct Key {
         GenArgs a;
-        unsigned gen0_grid, gen_grid[4], fin_grid;
+        unsigned gen0_grid, gen_grid, fin_grid;
     } key;
     std::memset(&key, 0, sizeof key);
     key.a = a;
     key.a.cond = 0;
     key.gen0_grid = gen0_grid;
-    for (int i = 0; i < 4; ++i)
-        key.gen_grid[i] = gen_grid[i];
+    key.gen_grid = gen_grid;
     key.fin_grid = fin_grid;
     static_assert(sizeof(Key) <= sizeof(G.key), "graph key too large");
     if (G.exec && G.key_size == sizeof key && std::memcmp(G.key, &key, sizeof key) == 0) {
@@ -837,24 +806,20 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, const unsigned g
     cudaGraphNode_t cnode;
     CCDK_CUDA_CHECK(cudaGraphAddNode(&cnode, G.graph, &f0, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    // body: the generation kernels (independent: one per split dimension, or
-    // one for all), then k_finish after all of them
-    cudaGraphNode_t gnodes[3];
-    int ng = 0;
-    for (int d = kGenSplit ? 0 : 3; d < (kGenSplit ? 3 : 4); ++d) {
-        kp.func = gen_kernel(d);
-        kp.gridDim = dim3(gen_grid[d]);
-        kp.blockDim = dim3(kGenBlock);
-        kp.sharedMemBytes = kGenSmem;
-        kp.kernelParams = params;
-        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnodes[ng++], body, nullptr, 0, &kp));
-    }
+    // body: the generation kernel, then its finish
+    kp.func = reinterpret_cast<void*>(k_generation);
+    kp.gridDim = dim3(gen_grid);
+    kp.blockDim = dim3(kGenBlock);
+    kp.sharedMemBytes = kGenSmem;
+    kp.kernelParams = params;
+    cudaGraphNode_t gnode;
+    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnode, body, nullptr, 0, &kp));
     kp.func = reinterpret_cast<void*>(k_finish);
     kp.gridDim = dim3(fin_grid);
     kp.blockDim = dim3(256);
     kp.sharedMemBytes = 0;
     cudaGraphNode_t fnode;
-    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, gnodes, ng, &kp));
+    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, &gnode, 1, &kp));
     CCDK_CUDA_CHECK(cudaGraphInstantiate(&G.exec, G.graph, 0));
     std::memcpy(G.key, &key, sizeof key);
     G.key_size = sizeof key;
@@ -934,18 +899,14 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
                                                                    a.zdiag);
     CCDK_LAUNCH_CHECK();
 
-    unsigned gen_grid[4];
-    for (int d = 0; d < 4; ++d) {
-        if (c.gen_blocks_per_sm[d] == 0) {
-            const void* f = gen_kernel(d);
-            CCDK_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenSmem));
-            CCDK_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            CCDK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.gen_blocks_per_sm[d], f, kGenBlock,
-                                                                          kGenSmem));
-            c.gen_blocks_per_sm[d] = std::max(1, c.gen_blocks_per_sm[d]);
-        }
-        gen_grid[d] = static_cast<unsigned>(c.gen_blocks_per_sm[d] * c.num_sms);
+    if (c.gen_blocks_per_sm == 0) {
+        CCDK_CUDA_CHECK(cudaFuncSetAttribute(k_generation, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenSmem));
+        CCDK_CUDA_CHECK(cudaFuncSetAttribute(k_generation, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CCDK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.gen_blocks_per_sm, k_generation, kGenBlock,
+                                                                      kGenSmem));
+        c.gen_blocks_per_sm = std::max(1, c.gen_blocks_per_sm);
     }
+    const unsigned gen_grid = static_cast<unsigned>(c.gen_blocks_per_sm * c.num_sms);
     const unsigned gen0_grid = static_cast<unsigned>(std::min<uint64_t>((n + kGenBlock - 1) / kGenBlock,
                                                                         uint64_t(8) * c.num_sms));
     const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
@@ -962,13 +923,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         k_finish<<<fin_grid, 256, 0, s>>>(a);
         for (;;) {
             for (int g = 0; g < 8; ++g) {
-                if (kGenSplit) {
-                    k_generation<0><<<gen_grid[0], kGenBlock, kGenSmem, s>>>(a);
-                    k_generation<1><<<gen_grid[1], kGenBlock, kGenSmem, s>>>(a);
-                    k_generation<2><<<gen_grid[2], kGenBlock, kGenSmem, s>>>(a);
-                } else {
-                    k_generation<3><<<gen_grid[3], kGenBlock, kGenSmem, s>>>(a);
-                }
+                k_generation<<<gen_grid, kGenBlock, kGenSmem, s>>>(a);
                 if (debug_enabled()) {
                     const cudaError_t e = cudaStreamSynchronize(s);
                     fprintf(stderr, "[ccdk narrow] k_generation: %s\n", cudaGetErrorString(e));
@@ -995,7 +950,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
     CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
     CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
-    c.narrow_launches += 3 + (kGenSplit ? 4 : 2) * host_sc->gen;
+    c.narrow_launches += 3 + 2 * host_sc->gen;
 #ifdef CCDK_STATS
     fprintf(stderr, "[ccdk stats] pairs with a live child %llu, with exactly one %llu\n", host_sc->vf_count,
             host_sc->next_n);

@@ -340,7 +340,7 @@ struct Ctx {
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
     DevBuf nscal;                      // NarrowScalars
     GenGraph gen_graph;
-    int gen_blocks_per_sm[4] = { 0, 0, 0, 0 }; // k_generation<DSEL> occupancy
+    int gen_blocks_per_sm = 0;
     uint64_t mem_probe_n = 0;          // narrow interval capacity probed for this many queries
     uint64_t mem_probe_cap = 0;
     EventPool events;
