@@ -447,7 +447,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "scene": WORKLOADS[args.workload], "primitives": k,
                    "parallelism": f"sweep-range shards x{world}"
