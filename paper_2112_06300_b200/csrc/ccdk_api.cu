@@ -449,7 +449,7 @@ struct BatchRun {
         double* seps = nullptr;
         if (cfg.min_sep_mode == CCDK_MINSEP_RELATIVE && n) {
             seps = grow<double>(c.q_sep, n);
-            launch_min_seps(c, qk, qp, n, cfg, seps);
+            launch_min_seps(c, qk, qp, n, cfg, seps, true);
             ++launches;
         }
         unsigned long long nvf = 0;
@@ -1161,10 +1161,12 @@ int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
         if (!n)
             return;
         uint8_t* dk = grow<uint8_t>(c.q_kind, n);
+        double* dref = grow<double>(c.q_points_ref, 24 * n);
         double* dp = grow<double>(c.q_points, 24 * n);
         double* ds = per_query_sep ? grow<double>(c.q_sep, n) : nullptr;
         h2d(c, dk, kind, n);
-        h2d(c, dp, points, 192 * n);
+        h2d(c, dref, points, 192 * n);
+        launch_records_to_internal(c, dref, n, dp);
         if (ds)
             h2d(c, ds, per_query_sep, 8 * n);
         NarrowIn ni;
@@ -1197,9 +1199,11 @@ int ccdk_narrow_phase_device(ccdk_ctx* ctx, const uint8_t* kind, const double* p
         stats->global_toi = INFINITY;
         if (!n)
             return;
+        double* dp = grow<double>(c.q_points, 24 * n);
+        launch_records_to_internal(c, points, n, dp);
         NarrowIn ni;
         ni.kind = kind;
-        ni.points = points;
+        ni.points = dp;
         ni.sep = per_query_sep;
         ni.n = n;
         ni.cfg = *cfg;
@@ -1309,7 +1313,7 @@ int ccdk_query_min_separations(ccdk_ctx* ctx, const uint8_t* kind, const double*
         double* dout = grow<double>(c.tmp[2], n);
         h2d(c, dk, kind, n);
         h2d(c, dp, points, 192 * n);
-        launch_min_seps(c, dk, dp, n, *cfg, dout);
+        launch_min_seps(c, dk, dp, n, *cfg, dout, false);
         d2h(c, out, dout, 8 * n);
         sync(c);
     });

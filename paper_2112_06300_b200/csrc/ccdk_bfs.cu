@@ -89,6 +89,15 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// 16-byte copies through L1 (.ca) or L2 only (.cg)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool l1)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if (l1)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -177,14 +186,14 @@ __global__ void __launch_bounds__(kGenBlock) k_gen0(GenArgs a)
             const unsigned qf = a.qf[q];
             const bool vf = !(qf & iv::kKindEE);
             const double sep = a.sep ? a.sep[q] : a.sep_default;
-            const iv::GlobalPts P { a.pts + 24ull * q };
+            const iv::GlobalPtsIL P { a.pts + 24ull * q };
             double cand = 0;
             bool zd = false, evald = false;
             int dim = -1, act;
             if (!(qf & iv::kKindExact)) {
                 act = iv::process_one<iv::Fast>(vf, P, bx, CUDART_INF, sep, a.cfg, cand, zd, dim, evald);
             } else {
-                const iv::Outcome o = iv::process_exact<iv::GlobalPts>(vf, P, bx, CUDART_INF, sep, a.cfg);
+                const iv::Outcome o = iv::process_exact<iv::GlobalPtsIL>(vf, P, bx, CUDART_INF, sep, a.cfg);
                 act = o.act;
                 cand = o.cand;
                 zd = o.zdiag;
@@ -277,6 +286,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     const unsigned long long c0 = sc->cur_pairs[0], c1 = sc->cur_pairs[1], c2 = sc->cur_pairs[2];
     const unsigned long long nb0 = (c0 + 31) >> 5, nb1 = (c1 + 31) >> 5, nb2 = (c2 + 31) >> 5;
     const unsigned long long nbatch = nb0 + nb1 + nb2;
+
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
     double* stage0 = gsm + wib * kWarpSmemDoubles;
@@ -296,13 +306,28 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
         if (bb < nbatch) {
             const BatchLoc L = locate(nb0, nb1, c0, c1, c2, bb);
             const unsigned long long i = L.i0 + lane;
+            // Query records through L1 (.ca) when any two neighbouring lanes
+            // of the batch share a query (dense BFS trees: C3/C5, measured
+            // 5-25% faster through L1), otherwise L2-only copies (.cg; C2/C4,
+            // where L1 allocation only costs: 8% faster).
+            const unsigned q_prev = __shfl_up_sync(0xffffffffu, q, 1); // all lanes: no divergence
+            const bool dup = lane > 0 && i < L.n && q_prev == q;
+#ifndef CCDK_L1_DUP
+#define CCDK_L1_DUP 1
+#endif
+#ifdef CCDK_L1
+            const bool l1_records = CCDK_L1;
+#else
+            const bool l1_records = __popc(__ballot_sync(0xffffffffu, dup)) >= CCDK_L1_DUP;
+#endif
             if (i < L.n) {
                 const Region& R = region(a, cb, L.d);
+                // the record's 12 (x0, x1) pairs (internal order), pair-major
                 double* coords = stage0 + st * kStageDoubles;
                 const double* src = a.pts + 24ull * q;
 #pragma unroll
-                for (int e = 0; e < 24; ++e)
-                    cp_async8(coords + 32 * e + lane, src + e);
+                for (int k = 0; k < 12; ++k)
+                    cp_async16(coords + 64 * k + 2 * lane, src + 2 * k, l1_records);
                 cp_async8(meta + 32 * kMT + lane, R.t + i);
                 cp_async8(meta + 32 * kMU + lane, R.u + i);
                 cp_async8(meta + 32 * kMV + lane, R.v + i);
@@ -403,7 +428,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                 if (alive[0] || alive[1]) {
                     // per-query separation (Relative min-separation mode only)
                     const double sep = a.sep ? a.sep[q] : a.sep_default;
-                    const iv::SmemPts P { stage0 + st * kStageDoubles + lane };
+                    const iv::SmemPts P { stage0 + st * kStageDoubles + 2 * lane };
                     iv::PairOutcome o;
                     if (!(qf & iv::kKindExact)) {
                         if (D == 0)
@@ -716,8 +741,8 @@ __global__ void __launch_bounds__(kClassifyBlock) k_classify_keys(
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 const double a = v0[3ull * pv[p] + c], b = v1[3ull * pv[p] + c];
-                st[24 * lane + 3 * p + c] = a;
-                st[24 * lane + 12 + 3 * p + c] = b;
+                st[24 * lane + 8 * c + 2 * p] = a; // internal order (iv::GlobalPtsIL)
+                st[24 * lane + 8 * c + 2 * p + 1] = b;
                 fast = fast && fabs(a) <= iv::kFastLimit && fabs(b) <= iv::kFastLimit;
             }
         qflags[q] = (k == CCDK_QUERY_EE ? iv::kKindEE : 0u) | (fast ? 0u : iv::kKindExact);
@@ -727,6 +752,20 @@ __global__ void __launch_bounds__(kClassifyBlock) k_classify_keys(
     double* out = pts + 24 * q0;
     for (unsigned i = lane; i < 24 * valid; i += 32)
         out[i] = st[i];
+}
+
+// Reference-order query records (API input) -> internal order: (x0, x1) of
+// point p, component c at 8c + 2p.
+__global__ void k_records_to_internal(const double* __restrict__ ref, unsigned long long n,
+                                      double* __restrict__ il)
+{
+    const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (i >= 24 * n)
+        return;
+    const unsigned long long q = i / 24;
+    const int e = static_cast<int>(i - 24 * q); // reference element
+    const int t = e / 12, r = e % 12;
+    il[24 * q + 8 * (r % 3) + 2 * (r / 3) + t] = ref[i];
 }
 
 __global__ void k_keys_to_ids(const unsigned long long* keys, unsigned long long n, int nb,
@@ -1067,6 +1106,14 @@ void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb, cons
         return;
     k_classify_keys<<<grid_for(n, kClassifyBlock), kClassifyBlock, 0, c.stream>>>(
         reinterpret_cast<const unsigned long long*>(keys), n, nb, v0, v1, nv, e, ne, f, kind, pts, qflags);
+    CCDK_LAUNCH_CHECK();
+}
+
+void launch_records_to_internal(Ctx& c, const double* ref, uint64_t n, double* il)
+{
+    if (!n)
+        return;
+    k_records_to_internal<<<grid_for(24 * n, 256), 256, 0, c.stream>>>(ref, n, il);
     CCDK_LAUNCH_CHECK();
 }
 

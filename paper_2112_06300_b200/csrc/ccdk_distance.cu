@@ -112,6 +112,7 @@ __device__ double segment_segment(V3 p0, V3 p1, V3 q0, V3 q1)
     return __dsqrt_rn(sqn(vsub(cp, cq)));
 }
 
+template <bool IL>
 __global__ void k_min_seps(const uint8_t* kind, const double* pts, unsigned long long n,
                            double fraction, int relative, double absolute, double* out)
 {
@@ -122,9 +123,11 @@ __global__ void k_min_seps(const uint8_t* kind, const double* pts, unsigned long
         out[i] = absolute;
         return;
     }
-    const double* P = pts + 24 * i; // t = 0 snapshot
-    const V3 a { P[0], P[1], P[2] }, b { P[3], P[4], P[5] }, c { P[6], P[7], P[8] },
-        d { P[9], P[10], P[11] };
+    const double* R = pts + 24 * i; // t = 0 snapshot
+    // element 3p + c of the t = 0 snapshot in either record order
+    auto P = [&](int e) { return IL ? R[8 * (e % 3) + 2 * (e / 3)] : R[e]; };
+    const V3 a { P(0), P(1), P(2) }, b { P(3), P(4), P(5) }, c { P(6), P(7), P(8) },
+        d { P(9), P(10), P(11) };
     const double d0 = kind[i] == CCDK_QUERY_EE ? segment_segment(a, b, c, d) : point_triangle(a, b, c, d);
     out[i] = __dmul_rn(fraction, d0);
 }
@@ -132,13 +135,14 @@ __global__ void k_min_seps(const uint8_t* kind, const double* pts, unsigned long
 } // namespace
 
 void launch_min_seps(Ctx& c, const uint8_t* kind, const double* pts, uint64_t n,
-                     const ccdk_pipeline_cfg& cfg, double* out)
+                     const ccdk_pipeline_cfg& cfg, double* out, bool internal)
 {
     if (!n)
         return;
-    k_min_seps<<<grid_for(n, 128), 128, 0, c.stream>>>(kind, pts, n, cfg.min_sep_fraction,
-                                                       cfg.min_sep_mode == CCDK_MINSEP_RELATIVE,
-                                                       cfg.narrow.min_separation, out);
+    auto k = internal ? k_min_seps<true> : k_min_seps<false>;
+    k<<<grid_for(n, 128), 128, 0, c.stream>>>(kind, pts, n, cfg.min_sep_fraction,
+                                              cfg.min_sep_mode == CCDK_MINSEP_RELATIVE,
+                                              cfg.narrow.min_separation, out);
     CCDK_LAUNCH_CHECK();
 }
 

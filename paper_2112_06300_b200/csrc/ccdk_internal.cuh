@@ -267,7 +267,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out);
 // narrow phase (ccdk_narrow.cu)
 struct NarrowIn {
     const uint8_t* kind = nullptr;   // device
-    const double* points = nullptr;  // device, n*24
+    const double* points = nullptr;  // device, n*24, internal order (iv::GlobalPtsIL)
     const double* sep = nullptr;     // device or null
     const uint32_t* qflags = nullptr; // device or null: per-query kind | exact-widening flags precomputed
     uint64_t n = 0;
@@ -294,9 +294,11 @@ void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
                           const uint32_t* e, uint64_t ne, const uint32_t* f, uint8_t* kind,
                           double* pts, uint32_t* qflags);
 // query_min_separations (pipeline.cpp:39-55) incl. the distances of
-// distance.cpp (ccdk_distance.cu)
+// distance.cpp (ccdk_distance.cu); internal: records in internal order
 void launch_min_seps(Ctx& c, const uint8_t* kind, const double* pts, uint64_t n,
-                     const ccdk_pipeline_cfg& cfg, double* out);
+                     const ccdk_pipeline_cfg& cfg, double* out, bool internal);
+// reference-order query records -> narrow-phase internal order
+void launch_records_to_internal(Ctx& c, const double* ref, uint64_t n, double* il);
 void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
                         const uint8_t* own_kind, const uint32_t* own_index, uint64_t nv,
                         uint64_t ne, uint64_t* ids);
@@ -334,7 +336,7 @@ struct Ctx {
     bool last_pairs_general = false;
 
     // queries / narrow phase
-    DevBuf q_kind, q_points, q_sep, q_flags, q_pflags;
+    DevBuf q_kind, q_points, q_points_ref, q_sep, q_flags, q_pflags;
     // interval records by split dimension (region) and generation parity
     DevBuf iv_qid[2][3], iv_t[2][3], iv_u[2][3], iv_v[2][3], iv_dep[2][3];
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;

@@ -116,15 +116,44 @@ struct Eval {
 // The hull starts from corner 0 like the reference; min/max of the remaining
 // corners is order-independent (bounds are never +/-0 after widening, and a
 // NaN operand is ignored by std::min/max unless it is the running value).
-// Coordinate sources: a global query record (24 doubles) or a lane's column
-// of a transposed shared-memory stage (element e at base[32 * e]).
-struct GlobalPts {
+// Coordinate sources.  Query records come in two layouts:
+//   reference (API) order — x0 of point p, component c at 3p + c, x1 at 12 + 3p + c
+//     (NarrowQuery::points_t0/points_t1, broadphase.hpp:26-35);
+//   narrow-phase internal order — (x0, x1) of point p, component c adjacent at
+//     8c + 2p, so one 16-byte load brings both snapshots of a coordinate.
+// pair(p, c) returns (x0, x1) of point p, component c; operator()(e) takes a
+// reference-order element index.
+struct GlobalPts { // reference order, global memory
     const double* __restrict__ p;
     __device__ __forceinline__ double operator()(int e) const { return __ldg(p + e); }
+    __device__ __forceinline__ double2 pair(int pt, int c) const
+    {
+        return make_double2(__ldg(p + 3 * pt + c), __ldg(p + 12 + 3 * pt + c));
+    }
 };
-struct SmemPts {
-    const double* p;
-    __device__ __forceinline__ double operator()(int e) const { return p[32 * e]; }
+struct GlobalPtsIL { // internal order, global memory (16-byte aligned records)
+    const double* __restrict__ p;
+    __device__ __forceinline__ double operator()(int e) const
+    {
+        const int t = e / 12, r = e % 12;
+        return __ldg(p + 8 * (r % 3) + 2 * (r / 3) + t);
+    }
+    __device__ __forceinline__ double2 pair(int pt, int c) const
+    {
+        return __ldg(reinterpret_cast<const double2*>(p + 8 * c + 2 * pt));
+    }
+};
+struct SmemPts { // internal order staged pair-major: pair k = 4c + p of lane l at [64 k + 2 l]
+    const double* p; // stage + 2 * lane
+    __device__ __forceinline__ double operator()(int e) const
+    {
+        const int t = e / 12, r = e % 12;
+        return p[64 * (4 * (r % 3) + r / 3) + t];
+    }
+    __device__ __forceinline__ double2 pair(int pt, int c) const
+    {
+        return *reinterpret_cast<const double2*>(p + 64 * (4 * c + pt));
+    }
 };
 
 // One component c of evaluate_box: the hull `rng` of the 8 corners and the
@@ -138,9 +167,9 @@ __device__ __forceinline__ void component(bool vf, const Pts& P, const Box& b, i
         I dl[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            x0[p] = P(3 * p + c);
-            const double x1 = P(12 + 3 * p + c);
-            const double d = __dsub_rn(x1, x0[p]); // point(x1) - point(x0): both bounds
+            const double2 xx = P.pair(p, c);
+            x0[p] = xx.x;
+            const double d = __dsub_rn(xx.y, x0[p]); // point(x1) - point(x0): both bounds
             dl[p] = { W::dn(d), W::up(d) };
         }
         double m0[4]; // corner midpoints at t = lo, indexed by (u bit) | (v bit) << 1
@@ -311,9 +340,9 @@ __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const Pair
     I dl[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        x0[p] = P(3 * p + c);
-        const double x1 = P(12 + 3 * p + c);
-        const double d = __dsub_rn(x1, x0[p]);
+        const double2 xx = P.pair(p, c);
+        x0[p] = xx.x;
+        const double d = __dsub_rn(xx.y, x0[p]);
         dl[p] = { W::dn(d), W::up(d) };
     }
     double mp[NU * NV]; // corner midpoints at the previous t sample

@@ -11,5 +11,5 @@ cfg = ck.PipelineConfig(inflation=0.01)
 reps = [rs.step(cfg) for _ in range(n + 2)][2:]
 med = {k: round(statistics.median(r.device[k] for r in reps), 3) for k in reps[0].device if k.startswith("ms_")}
 r = reps[-1]
-print((os.environ.get("CCDK_LIB") or "x/default/x").split("/")[-2], w, "toi", r.toi.toi, "splits", r.device["total_splits"],
+print((os.environ.get("CCDK_LIB") or "x/default/x").split("/")[-2], w, "toi", r.toi.toi, "q", r.query_count, "gens", r.device["generations"], "splits", r.device["total_splits"],
       "evals", r.device["evaluations"], med)
