@@ -200,6 +200,8 @@ __device__ __forceinline__ QuantAxis quant_axis(const unsigned* qb, int a)
     QuantAxis q { lo, 0.0f };
     if (isfinite(lo) && isfinite(hi) && isfinite(ext) && ext > 0.0f)
         q.s = __fdiv_rn(32767.0f, ext);
+    if (!isfinite(q.s)) // denormal extent
+        q.s = 0.0f;
     return q; // s == 0: every box quantises to 0 (the filter passes all)
 }
 __device__ __forceinline__ unsigned quant_dn(QuantAxis q, float x)

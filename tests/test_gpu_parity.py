@@ -531,3 +531,41 @@ def test_c4_full_size_bit_exact(ctx):
     etoi, efl, st = r.narrow_phase(kind, pts, NarrowConfig().to_c())
     assert_bits(toi, etoi)
     np.testing.assert_array_equal(flags, efl)
+
+
+def test_broad_phase_quantised_filter_extremes(ctx, ref):
+    """The sweep's 15-bit quantised pre-filter must stay a superset of the
+    exact fp32 test whatever the coordinates: touching boxes (max == min),
+    -0/+0, one huge box stretching the quantisation range, 1e30 magnitudes,
+    +-FLT_MAX and infinities (round_up_reduced overflow), denormals, and a
+    scene where every box is identical (zero extent)."""
+    f32max = np.float32(3.4028235e38)
+    cases = []
+    b, s = random_boxes(77, 400)
+    b.min_corner[0] = [-1e30, -1e30, -1e30]   # one box spans the whole range
+    b.max_corner[0] = [1e30, 1e30, 1e30]
+    cases.append((b, s))
+    b, s = random_boxes(78, 300)
+    b.max_corner[:, 1] = b.min_corner[:, 1]   # zero extent on one axis, touching pairs
+    b.min_corner[::7] = -0.0
+    b.max_corner[::7] = 0.0
+    cases.append((b, s))
+    b, s = random_boxes(79, 300)
+    b.min_corner[:5] = -np.inf
+    b.max_corner[5:10] = np.inf
+    b.min_corner[10:15] = -f32max
+    b.max_corner[15:20] = f32max
+    cases.append((b, s))
+    b, s = random_boxes(80, 200)
+    b.min_corner[:] = b.min_corner[0]
+    b.max_corner[:] = b.max_corner[0]
+    cases.append((b, s))
+    b, s = random_boxes(81, 300)
+    b.min_corner *= np.float32(1e-40)         # denormal coordinates
+    b.max_corner *= np.float32(1e-40)
+    cases.append((b, s))
+    for b, s in cases:
+        for method in (abi.BROAD_STQ, abi.BROAD_SAP):
+            got = ck._broad(method, b, s, None, None, ctx)
+            exp, _, _ = ref.broad(method, b.as_tuple(), s)
+            np.testing.assert_array_equal(got, exp)
