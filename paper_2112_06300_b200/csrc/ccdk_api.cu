@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <memory>
 
@@ -788,6 +789,8 @@ int ccdk_ctx_destroy(ccdk_ctx* ctx)
         cudaStreamSynchronize(ctx->stream);
         if (ctx->own_stream)
             cudaStreamDestroy(ctx->stream);
+        if (ctx->copy_stream)
+            cudaStreamDestroy(ctx->copy_stream);
         delete ctx;
     });
 }
@@ -1164,24 +1167,156 @@ int ccdk_narrow_phase(ccdk_ctx* ctx, const uint8_t* kind, const double* points,
         double* dref = grow<double>(c.q_points_ref, 24 * n);
         double* dp = grow<double>(c.q_points, 24 * n);
         double* ds = per_query_sep ? grow<double>(c.q_sep, n) : nullptr;
-        h2d(c, dk, kind, n);
-        h2d(c, dref, points, 192 * n);
-        launch_records_to_internal(c, dref, n, dp);
-        if (ds)
-            h2d(c, ds, per_query_sep, 8 * n);
-        NarrowIn ni;
-        ni.kind = dk;
-        ni.points = dp;
-        ni.sep = ds;
-        ni.n = n;
-        ni.cfg = *cfg;
-        ni.queue_capacity = queue_capacity;
-        NarrowOut no;
-        narrow_phase(c, ni, no);
-        d2h(c, toi, no.toi, 8 * n);
-        d2h(c, flags, no.flags, n);
+        // Large batches from pinned host memory are streamed: chunk i+1's
+        // upload (copy stream) overlaps chunk i's narrow phase.  Per-query
+        // results are partition-independent (narrowphase.hpp:93-96) and the
+        // per-generation queue sizes of the chunks add up (gen_acc), so the
+        // results and stats equal one run; a bounded queue capacity needs the
+        // whole batch in one BFS (its overflow test is global) and is not
+        // chunked.
+        constexpr uint64_t kMinChunk = uint64_t(1) << 21;
+        auto pinned = [](const void* p) {
+            cudaPointerAttributes at {};
+            return p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        };
+        const bool chunked = n >= 2 * kMinChunk && queue_capacity == UINT64_MAX && pinned(points) && pinned(kind)
+            && (!per_query_sep || pinned(per_query_sep));
+        // ~3 chunks: the first upload is exposed, every chunk adds a BFS's
+        // fixed per-generation costs (measured optimum for 10M queries)
+        const uint64_t kChunk = std::max<uint64_t>(kMinChunk, (n + 2) / 3);
+        if (!chunked) {
+            h2d(c, dk, kind, n);
+            h2d(c, dref, points, 192 * n);
+            launch_records_to_internal(c, dref, n, dp);
+            if (ds)
+                h2d(c, ds, per_query_sep, 8 * n);
+            NarrowIn ni;
+            ni.kind = dk;
+            ni.points = dp;
+            ni.sep = ds;
+            ni.n = n;
+            ni.cfg = *cfg;
+            ni.queue_capacity = queue_capacity;
+            NarrowOut no;
+            narrow_phase(c, ni, no);
+            d2h(c, toi, no.toi, 8 * n);
+            d2h(c, flags, no.flags, n);
+            sync(c);
+            *stats = no.stats;
+            return;
+        }
+        if (!c.copy_stream)
+            CCDK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+        const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+        std::vector<cudaEvent_t> up(nchunks, nullptr), done(nchunks, nullptr);
+        cudaEvent_t t0 = nullptr;
+        if (debug_enabled()) {
+            CCDK_CUDA_CHECK(cudaEventCreate(&t0));
+            CCDK_CUDA_CHECK(cudaEventRecord(t0, c.stream));
+            CCDK_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, t0, 0));
+        }
+        const auto h0 = std::chrono::steady_clock::now();
+        // one upload in flight ahead of the chunk being computed: the copy
+        // engine serves copies in order, so a deeper queue would hold back
+        // the narrow phase's own small read-backs until every upload is done
+        auto upload = [&](uint64_t i) {
+            const uint64_t lo = i * kChunk, cnt = std::min<uint64_t>(kChunk, n - lo);
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(dk + lo, kind + lo, cnt, cudaMemcpyHostToDevice, c.copy_stream));
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(dref + 24 * lo, points + 24 * lo, 192 * cnt, cudaMemcpyHostToDevice,
+                                            c.copy_stream));
+            if (ds)
+                CCDK_CUDA_CHECK(cudaMemcpyAsync(ds + lo, per_query_sep + lo, 8 * cnt, cudaMemcpyHostToDevice,
+                                                c.copy_stream));
+            CCDK_CUDA_CHECK(cudaEventCreateWithFlags(&up[i], debug_enabled() ? 0 : cudaEventDisableTiming));
+            CCDK_CUDA_CHECK(cudaEventRecord(up[i], c.copy_stream));
+        };
+        upload(0);
+        if (debug_enabled()) {
+            cudaPointerAttributes at {};
+            cudaPointerGetAttributes(&at, points);
+            std::fprintf(stderr, "[ccdk chunks] %llu uploads enqueued in %.3f ms (points memory type %d)\n",
+                         (unsigned long long)nchunks,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(),
+                         (int)at.type);
+        }
+        double* rtoi = grow<double>(c.chunk_toi, n);
+        uint8_t* rflags = grow<uint8_t>(c.chunk_flags, n);
+        uint8_t* ck_kind = grow<uint8_t>(c.chunk_kind, kChunk);
+        double* ck_pts = grow<double>(c.chunk_points, 24 * kChunk);
+        double* ck_sep = ds ? grow<double>(c.chunk_sep, kChunk) : nullptr;
+        ccdk_narrow_stats tot {};
+        tot.global_toi = INFINITY;
+        c.gen_acc.clear();
+        c.gen_acc_keep = true;
+        try {
+            for (uint64_t i = 0; i < nchunks; ++i) {
+                const uint64_t lo = i * kChunk, cnt = std::min<uint64_t>(kChunk, n - lo);
+                if (i + 1 < nchunks)
+                    upload(i + 1);
+                CCDK_CUDA_CHECK(cudaStreamWaitEvent(c.stream, up[i], 0));
+                // the chunk goes to fixed addresses, so the generation graph
+                // (keyed on its kernel arguments) is reused across chunks
+                launch_records_to_internal(c, dref + 24 * lo, cnt, ck_pts);
+                launch_copy_device(c, dk + lo, ck_kind, cnt);
+                if (ds)
+                    launch_copy_device(c, ds + lo, ck_sep, 8 * cnt);
+                NarrowIn ni;
+                ni.kind = ck_kind;
+                ni.points = ck_pts;
+                ni.sep = ds ? ck_sep : nullptr;
+                ni.n = cnt;
+                ni.cfg = *cfg;
+                NarrowOut no;
+                narrow_phase(c, ni, no);
+                // results gathered on the device; one read-back at the end (a
+                // device-to-pageable copy per chunk would block the host)
+                launch_copy_device(c, no.toi, rtoi + lo, 8 * cnt);
+                launch_copy_device(c, no.flags, rflags + lo, cnt);
+                if (debug_enabled()) {
+                    CCDK_CUDA_CHECK(cudaEventCreate(&done[i]));
+                    CCDK_CUDA_CHECK(cudaEventRecord(done[i], c.stream));
+                    std::fprintf(stderr, "[ccdk chunk %llu] host %.2f ms, narrow device %.2f ms, gens %llu\n",
+                                 (unsigned long long)i,
+                                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(),
+                                 no.stats.device_ms, (unsigned long long)no.stats.generations);
+                }
+                tot.global_toi = std::min(tot.global_toi, no.stats.global_toi);
+                tot.total_splits += no.stats.total_splits;
+                tot.evaluations += no.stats.evaluations;
+                tot.split_actions += no.stats.split_actions;
+                tot.generations = std::max(tot.generations, no.stats.generations);
+                tot.device_ms += no.stats.device_ms;
+            }
+        } catch (...) {
+            c.gen_acc_keep = false;
+            for (auto e : up)
+                if (e)
+                    cudaEventDestroy(e);
+            throw;
+        }
+        c.gen_acc_keep = false;
+        d2h(c, toi, rtoi, 8 * n);
+        d2h(c, flags, rflags, n);
         sync(c);
-        *stats = no.stats;
+        if (debug_enabled()) {
+            for (uint64_t i = 0; i < nchunks; ++i) {
+                float mu = -1, md = -1;
+                const cudaError_t e1 = cudaEventElapsedTime(&mu, t0, up[i]);
+                const cudaError_t e2 = cudaEventElapsedTime(&md, t0, done[i]);
+                if (e1 || e2)
+                    std::fprintf(stderr, "[ccdk chunk] event times: %s / %s\n", cudaGetErrorString(e1),
+                                 cudaGetErrorString(e2));
+                std::fprintf(stderr, "[ccdk chunk %llu] uploaded at %.2f ms, narrowed at %.2f ms\n",
+                             (unsigned long long)i, mu, md);
+                cudaEventDestroy(done[i]);
+            }
+            cudaEventDestroy(t0);
+        }
+        for (auto e : up)
+            cudaEventDestroy(e);
+        for (uint64_t v : c.gen_acc)
+            tot.peak_queue = std::max<uint64_t>(tot.peak_queue, v);
+        *stats = tot;
     });
 }
 

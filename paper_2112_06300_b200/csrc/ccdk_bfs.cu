@@ -31,6 +31,7 @@ namespace {
 constexpr unsigned kNoGen = 0xffffffffu;
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr int kGenBlock = 128;
+constexpr unsigned kMaxGens = 4096; // > the 4000-generation guard
 #ifndef CCDK_GEN_MINB
 #define CCDK_GEN_MINB 3
 #endif
@@ -63,13 +64,12 @@ struct GenArgs {
     unsigned* exh_gen;
     uint8_t* zdiag;
     unsigned* dirty;                 // queries whose ToI dropped (duplicates allowed)
-    unsigned long long dirty_cap;    // beyond it k_finish refreshes every query
-    unsigned long long nq;           // queries in this run
     Region reg[2][3];                // [generation parity][split dimension]
     unsigned long long cap_pairs;    // records per region buffer
     unsigned long long sem_cap;
     NarrowScalars* sc;
     cudaGraphConditionalHandle cond; // WHILE node of the generation graph
+    unsigned long long* gen_sizes;   // compacted queue size per generation (kMaxGens entries)
 };
 
 __device__ __forceinline__ unsigned long long dbits(double x)
@@ -114,7 +114,7 @@ __device__ __forceinline__ void record_collision(const GenArgs& a, unsigned q, d
 {
     atomicMin(&a.toi[q], dbits(cand));
     const unsigned long long slot = atomicAdd(&a.sc->dirty_n, 1ull);
-    if (slot < a.dirty_cap)
+    if (slot < a.sc->dirty_cap)
         a.dirty[slot] = q;
     if (zd)
         a.zdiag[q] = 1;
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kGenBlock) k_gen0(GenArgs a)
     NarrowScalars* sc = a.sc;
     const unsigned lane = threadIdx.x & 31;
     unsigned evals = 0, split_actions = 0;
-    const unsigned long long n = a.nq;
+    const unsigned long long n = sc->nq;
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
     // warp-uniform trip count (the append is warp-collective)
     const unsigned long long n_up = (n + 31) & ~31ull;
@@ -512,8 +512,8 @@ __global__ void k_finish(GenArgs a)
         return;
     }
     const unsigned long long nd = sc->dirty_n;
-    const bool all = nd > a.dirty_cap; // list overflowed: refresh every query
-    const unsigned long long m = all ? a.nq : nd;
+    const bool all = nd > sc->dirty_cap; // list overflowed: refresh every query
+    const unsigned long long m = all ? sc->nq : nd;
     for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
         const unsigned q = all ? static_cast<unsigned>(i) : a.dirty[i];
@@ -532,6 +532,8 @@ __global__ void k_finish(GenArgs a)
     const unsigned long long compacted = sc->cur_n - sc->dropped;
     if (compacted > sc->peak)
         sc->peak = compacted;
+    if (sc->gen < kMaxGens)
+        a.gen_sizes[sc->gen] = compacted;
     if (compacted > a.sem_cap)
         sc->sem_overflow = 1;
     unsigned long long raw_next = 0;
@@ -558,6 +560,21 @@ __global__ void k_finish(GenArgs a)
     __threadfence();
     if (a.cond)
         cudaGraphSetConditional(a.cond, sc->cont ? 1u : 0u);
+}
+
+__global__ void k_init_scalars(NarrowScalars* sc, unsigned long long n)
+{
+    unsigned long long* w = reinterpret_cast<unsigned long long*>(sc);
+    for (unsigned i = threadIdx.x; i < sizeof(NarrowScalars) / 8; i += blockDim.x)
+        w[i] = 0;
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        sc->cur_n = n;
+        sc->nq = n;
+        sc->dirty_cap = 2 * n;
+        sc->cont = 1;
+        sc->global_toi_bits = kInfBits;
+    }
 }
 
 __device__ __forceinline__ uint32_t query_flags(uint8_t kind, const double* pts)
@@ -911,8 +928,6 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     a.exh_gen = grow<unsigned>(c.exh_gen, n);
     a.zdiag = grow<uint8_t>(c.zdiag, n);
     a.dirty = grow<unsigned>(c.dirty, 2 * n);
-    a.dirty_cap = 2 * n;
-    a.nq = n;
     for (int b = 0; b < 2; ++b)
         for (int d = 0; d < 3; ++d) {
             Region& R = a.reg[b][d];
@@ -925,13 +940,12 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     a.cap_pairs = cap_pairs;
     a.sem_cap = in.queue_capacity;
     a.sc = static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars)));
+    a.gen_sizes = grow<unsigned long long>(c.gen_sizes, kMaxGens);
 
-    NarrowScalars* init = static_cast<NarrowScalars*>(c.pin_init.ensure(sizeof(NarrowScalars)));
-    std::memset(init, 0, sizeof(NarrowScalars));
-    init->cur_n = n;
-    init->cont = 1;
-    init->global_toi_bits = kInfBits;
-    CCDK_CUDA_CHECK(cudaMemcpyAsync(a.sc, init, sizeof(NarrowScalars), cudaMemcpyHostToDevice, s));
+    // scalars initialised by a kernel, not a host-to-device copy: the copy
+    // engine serves H2D copies in order across streams, so during a chunked
+    // upload a tiny copy here would wait behind all the bulk uploads
+    k_init_scalars<<<1, 32, 0, s>>>(a.sc, n);
     const dim3 ig = grid_for(n, 256);
     k_init_queries<<<std::min<unsigned>(ig.x, 65535u), 256, 0, s>>>(n, kind, pts, qflags ? nullptr : a.qf,
                                                                    a.toi, a.snap, a.splits, a.exh_gen,
@@ -988,6 +1002,8 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     CCDK_LAUNCH_CHECK();
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
     CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
+    unsigned long long* host_gs = static_cast<unsigned long long*>(c.pin_gens.ensure(kMaxGens * 8));
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(host_gs, a.gen_sizes, kMaxGens * 8, cudaMemcpyDeviceToHost, s));
     CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
     c.narrow_launches += 3 + 2 * host_sc->gen;
 #ifdef CCDK_STATS
@@ -1006,6 +1022,14 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     const double g = __builtin_bit_cast(double, static_cast<uint64_t>(host_sc->global_toi_bits));
     st.global_toi = st.overflow ? INFINITY : std::min(st.global_toi, g);
     st.peak_queue = std::max<uint64_t>(st.peak_queue, std::max<uint64_t>(host_sc->peak, n));
+    // per-generation queue sizes of independent query subsets add up: the
+    // combined peak of a split run (physical halving, chunked upload) is the
+    // max over generations of the sums, exactly the reference's peak_queue
+    const uint64_t ng = std::min<uint64_t>(host_sc->gen, kMaxGens);
+    if (c.gen_acc.size() < ng)
+        c.gen_acc.resize(ng, 0);
+    for (uint64_t g = 0; g < ng; ++g)
+        c.gen_acc[g] += host_gs[g];
     st.total_splits += host_sc->total_splits;
     st.evaluations += host_sc->evaluations;
     st.split_actions += host_sc->split_actions;
@@ -1041,6 +1065,8 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     const uint64_t n = in.n;
     out.toi = grow<double>(c.out_toi, n);
     out.flags = grow<uint8_t>(c.out_flags, n);
+    if (!c.gen_acc_keep)
+        c.gen_acc.clear();
     cudaEvent_t e0 = c.events.get(EventPool::kNarrow), e1 = c.events.get(EventPool::kNarrow + 1);
     CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
     if (n > 0 && n > in.queue_capacity) {
@@ -1069,6 +1095,10 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     st.device_ms = ms;
     if (st.overflow) {
         st.global_toi = INFINITY;
+    } else if (n > 0) {
+        st.peak_queue = 0;
+        for (uint64_t v : c.gen_acc)
+            st.peak_queue = std::max<uint64_t>(st.peak_queue, v);
     }
     out.stats = st;
     out.launches = c.narrow_launches;
@@ -1106,6 +1136,37 @@ void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb, cons
         return;
     k_classify_keys<<<grid_for(n, kClassifyBlock), kClassifyBlock, 0, c.stream>>>(
         reinterpret_cast<const unsigned long long*>(keys), n, nb, v0, v1, nv, e, ne, f, kind, pts, qflags);
+    CCDK_LAUNCH_CHECK();
+}
+
+// Device-to-device copy by a kernel: a cudaMemcpyAsync would go through a
+// copy engine and queue behind a concurrent bulk upload.
+__global__ void k_copy_bytes(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                             unsigned long long bytes)
+{
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    const unsigned long long n8 = bytes / 8;
+    const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(src);
+    unsigned long long* d8 = reinterpret_cast<unsigned long long*>(dst);
+    const bool aligned = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 8 == 0;
+    unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (aligned) {
+        for (unsigned long long j = i; j < n8; j += stride)
+            d8[j] = s8[j];
+        for (unsigned long long j = 8 * n8 + i; j < bytes; j += stride)
+            dst[j] = src[j];
+    } else {
+        for (unsigned long long j = i; j < bytes; j += stride)
+            dst[j] = src[j];
+    }
+}
+
+void launch_copy_device(Ctx& c, const void* src, void* dst, uint64_t bytes)
+{
+    if (!bytes)
+        return;
+    k_copy_bytes<<<std::min<unsigned>(grid_for(bytes / 8 + 1, 256).x, 4 * c.num_sms), 256, 0, c.stream>>>(
+        static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst), bytes);
     CCDK_LAUNCH_CHECK();
 }
 

@@ -199,6 +199,8 @@ struct NarrowScalars {
     unsigned long long any_flags;   // OR of per-query flags
     unsigned long long vf_count;
     unsigned long long gen_limit;   // set when the generation guard trips
+    unsigned long long nq;            // queries of this run (device-side so the graph is size-independent)
+    unsigned long long dirty_cap;     // dirty-list capacity; beyond it every query is refreshed
     unsigned long long cur_pairs[3];  // split records per region in the current generation
     unsigned long long next_pairs[3]; // append cursors of the next generation
 };
@@ -297,6 +299,8 @@ void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
 // distance.cpp (ccdk_distance.cu); internal: records in internal order
 void launch_min_seps(Ctx& c, const uint8_t* kind, const double* pts, uint64_t n,
                      const ccdk_pipeline_cfg& cfg, double* out, bool internal);
+// device-to-device copy by a kernel (stays off the copy engines)
+void launch_copy_device(Ctx& c, const void* src, void* dst, uint64_t bytes);
 // reference-order query records -> narrow-phase internal order
 void launch_records_to_internal(Ctx& c, const double* ref, uint64_t n, double* il);
 void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
@@ -342,6 +346,13 @@ struct Ctx {
     DevBuf toi_live, toi_snap, splits, exh_gen, zdiag, dirty, out_toi, out_flags;
     DevBuf nscal;                      // NarrowScalars
     GenGraph gen_graph;
+    DevBuf gen_sizes;                  // per-generation compacted queue sizes of a run
+    PinnedBuf pin_gens;
+    std::vector<uint64_t> gen_acc;     // summed over the runs of one narrow phase (exact combined peak)
+    bool gen_acc_keep = false;         // chunked callers accumulate across narrow_phase calls
+    cudaStream_t copy_stream = nullptr; // H2D of the next chunk while a chunk is narrow-phased
+    DevBuf chunk_toi, chunk_flags;     // per-query results gathered over the chunks
+    DevBuf chunk_kind, chunk_points, chunk_sep; // the chunk being narrow-phased (fixed addresses)
     int gen_blocks_per_sm = 0;
     uint64_t mem_probe_n = 0;          // narrow interval capacity probed for this many queries
     uint64_t mem_probe_cap = 0;

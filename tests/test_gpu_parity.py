@@ -569,3 +569,23 @@ def test_broad_phase_quantised_filter_extremes(ctx, ref):
             got = ck._broad(method, b, s, None, None, ctx)
             exp, _, _ = ref.broad(method, b.as_tuple(), s)
             np.testing.assert_array_equal(got, exp)
+
+
+def test_chunked_upload_equals_single_run(ctx):
+    """ccdk_narrow_phase streams large batches from pinned memory in chunks
+    (upload of chunk i+1 overlapping chunk i's BFS).  Results and stats —
+    including the peak queue size, combined across chunks per generation —
+    must equal the single-run path (same batch from pageable memory)."""
+    import torch
+    qb = scenes.mixed_queries(4_500_000, seed=1003, every=10000, n_exhaust=2)
+    single = ck.narrow_phase(qb, ctx=ctx)  # pageable numpy -> one run
+    kt = torch.from_numpy(qb.kind).pin_memory()
+    pt = torch.from_numpy(qb.points).pin_memory()
+    chunked = ck.narrow_phase(scenes.QueryBatch(kt.numpy(), pt.numpy()), ctx=ctx)
+    assert_bits(chunked.toi, single.toi)
+    np.testing.assert_array_equal(chunked.flags, single.flags)
+    assert chunked.total_splits == single.total_splits
+    assert chunked.evaluations == single.evaluations
+    assert chunked.peak_queue == single.peak_queue
+    assert chunked.generations == single.generations
+    assert bits(np.array([chunked.global_toi]))[0] == bits(np.array([single.global_toi]))[0]
