@@ -230,7 +230,9 @@ __global__ void k_permute(const float* bmin, const float* bmax, const uint4* vid
     const float4 b = make_float4(bmin[a1 * k + s], bmax[a1 * k + s], bmin[a2 * k + s], bmax[a2 * k + s]);
     sbox[p] = b;
     const QuantAxis q1 = quant_axis(qb, a1), q2 = quant_axis(qb, a2);
-    sq[p] = make_uint2(quant_dn(q1, b.x) | (quant_dn(q2, b.z) << 16), quant_up(q1, b.y) | (quant_up(q2, b.w) << 16));
+    // hi word stored with the guard bits set (see qhit)
+    sq[p] = make_uint2(quant_dn(q1, b.x) | (quant_dn(q2, b.z) << 16),
+                       quant_up(q1, b.y) | (quant_up(q2, b.w) << 16) | 0x80008000u);
     svid[p] = vids[s];
     if (sraw)
         sraw[p] = raw ? raw[s] : static_cast<uint32_t>(s);
@@ -487,11 +489,12 @@ __device__ __forceinline__ void push_hit(unsigned* hits, unsigned& nh, bool h, u
 // Quantised 2-axis overlap (superset of the exact test): per 16-bit lane,
 // (0x8000 + a) - b keeps bit 15 iff a >= b (15-bit values: no borrow across
 // lanes), so one subtract checks both axes of one inequality.
+// Both operands' hi words carry the guard bits already (set at quantisation).
 constexpr unsigned kGuard = 0x80008000u;
 __device__ __forceinline__ bool qhit(unsigned m_hi_g, unsigned m_lo, uint2 o)
 {
-    const unsigned x1 = m_hi_g - o.x;          // o.qmin <= m.qmax
-    const unsigned x2 = (o.y | kGuard) - m_lo; // m.qmin <= o.qmax
+    const unsigned x1 = m_hi_g - o.x; // o.qmin <= m.qmax
+    const unsigned x2 = o.y - m_lo;   // m.qmin <= o.qmax
     return (x1 & x2 & kGuard) == kGuard;
 }
 
@@ -502,7 +505,7 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
     const float4 mb = a.sbox[p];
     const uint4 mv = a.svid[p];
     const uint2 mq = a.sq[p];
-    const unsigned m_hi_g = mq.y | kGuard, m_lo = mq.x;
+    const unsigned m_hi_g = mq.y, m_lo = mq.x;
     unsigned nh = 0;             // warp-uniform
     unsigned long long j0 = jb;  // warp-uniform stride base
     // kUnroll full strides per iteration: all loads in flight before the
