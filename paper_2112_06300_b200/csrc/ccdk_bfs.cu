@@ -32,6 +32,10 @@ constexpr unsigned kNoGen = 0xffffffffu;
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr int kGenBlock = 128;
 constexpr unsigned kMaxGens = 4096; // > the 4000-generation guard
+#ifndef CCDK_GEN_UNROLL
+#define CCDK_GEN_UNROLL 8
+#endif
+constexpr int kGenUnroll = CCDK_GEN_UNROLL; // generations per WHILE iteration of the graph
 #ifndef CCDK_GEN_MINB
 #define CCDK_GEN_MINB 3
 #endif
@@ -862,20 +866,26 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_gri
     cudaGraphNode_t cnode;
     CCDK_CUDA_CHECK(cudaGraphAddNode(&cnode, G.graph, &f0, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    // body: the generation kernel, then its finish
-    kp.func = reinterpret_cast<void*>(k_generation);
-    kp.gridDim = dim3(gen_grid);
-    kp.blockDim = dim3(kGenBlock);
-    kp.sharedMemBytes = kGenSmem;
-    kp.kernelParams = params;
-    cudaGraphNode_t gnode;
-    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnode, body, nullptr, 0, &kp));
-    kp.func = reinterpret_cast<void*>(k_finish);
-    kp.gridDim = dim3(fin_grid);
-    kp.blockDim = dim3(256);
-    kp.sharedMemBytes = 0;
-    cudaGraphNode_t fnode;
-    CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, &gnode, 1, &kp));
+    // body: kGenUnroll x (generation kernel -> its finish), a chain; once a
+    // finish clears `cont` the rest of the chain exits at once, and the
+    // loop condition is the last finish's value (fewer conditional-node
+    // evaluations per generation)
+    cudaGraphNode_t prev = nullptr;
+    for (int u = 0; u < kGenUnroll; ++u) {
+        kp.func = reinterpret_cast<void*>(k_generation);
+        kp.gridDim = dim3(gen_grid);
+        kp.blockDim = dim3(kGenBlock);
+        kp.sharedMemBytes = kGenSmem;
+        kp.kernelParams = params;
+        cudaGraphNode_t gnode, fnode;
+        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnode, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+        kp.func = reinterpret_cast<void*>(k_finish);
+        kp.gridDim = dim3(fin_grid);
+        kp.blockDim = dim3(256);
+        kp.sharedMemBytes = 0;
+        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, &gnode, 1, &kp));
+        prev = fnode;
+    }
     CCDK_CUDA_CHECK(cudaGraphInstantiate(&G.exec, G.graph, 0));
     std::memcpy(G.key, &key, sizeof key);
     G.key_size = sizeof key;
@@ -1005,7 +1015,9 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     unsigned long long* host_gs = static_cast<unsigned long long*>(c.pin_gens.ensure(kMaxGens * 8));
     CCDK_CUDA_CHECK(cudaMemcpyAsync(host_gs, a.gen_sizes, kMaxGens * 8, cudaMemcpyDeviceToHost, s));
     CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
-    c.narrow_launches += 3 + 2 * host_sc->gen;
+    // k_init_scalars, k_init_queries, k_gen0 + finish, the unrolled loop's
+    // pairs (whole iterations), k_outputs
+    c.narrow_launches += 5 + 2 * kGenUnroll * ((host_sc->gen + kGenUnroll - 2) / kGenUnroll);
 #ifdef CCDK_STATS
     fprintf(stderr, "[ccdk stats] pairs with a live child %llu, with exactly one %llu\n", host_sc->vf_count,
             host_sc->next_n);
