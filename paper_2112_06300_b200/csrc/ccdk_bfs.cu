@@ -36,6 +36,10 @@ constexpr unsigned kMaxGens = 4096; // > the 4000-generation guard
 #define CCDK_GEN_UNROLL 8
 #endif
 constexpr int kGenUnroll = CCDK_GEN_UNROLL; // generations per WHILE iteration of the graph
+#ifndef CCDK_PDL
+#define CCDK_PDL 1
+#endif
+constexpr bool kUsePdl = CCDK_PDL != 0; // programmatic dependent launch inside the generation chain
 #ifndef CCDK_GEN_MINB
 #define CCDK_GEN_MINB 3
 #endif
@@ -281,6 +285,7 @@ __device__ __forceinline__ iv::PairOutcome eval_pair(bool vf, const iv::SmemPts&
 
 __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs a)
 {
+    cudaGridDependencySynchronize(); // PDL: the previous finish has completed (no-op otherwise)
     extern __shared__ double gsm[];
     NarrowScalars* sc = a.sc;
     if (!sc->cont)
@@ -509,6 +514,7 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
 // block) the queue bookkeeping of narrowphase.cpp:299-304.
 __global__ void k_finish(GenArgs a)
 {
+    cudaGridDependencySynchronize(); // PDL: the generation kernel has completed (no-op otherwise)
     NarrowScalars* sc = a.sc;
     if (!sc->cont) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && a.cond)
@@ -870,6 +876,15 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_gri
     // finish clears `cont` the rest of the chain exits at once, and the
     // loop condition is the last finish's value (fewer conditional-node
     // evaluations per generation)
+    // Edges inside the chain are programmatic (PDL): a kernel is launched as
+    // soon as every block of its predecessor has started, and waits in
+    // cudaGridDependencySynchronize() for the predecessor's completion and
+    // memory, so launch latency overlaps the predecessor's tail.  Safe: the
+    // predecessor's blocks are all running by then, so they finish whatever
+    // the early blocks occupy.
+    cudaGraphEdgeData pdl {};
+    pdl.from_port = cudaGraphKernelNodePortLaunchCompletion;
+    pdl.type = cudaGraphDependencyTypeProgrammatic;
     cudaGraphNode_t prev = nullptr;
     for (int u = 0; u < kGenUnroll; ++u) {
         kp.func = reinterpret_cast<void*>(k_generation);
@@ -878,12 +893,15 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_gri
         kp.sharedMemBytes = kGenSmem;
         kp.kernelParams = params;
         cudaGraphNode_t gnode, fnode;
-        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnode, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&gnode, body, nullptr, 0, &kp));
+        if (prev)
+            CCDK_CUDA_CHECK(cudaGraphAddDependencies_v2(body, &prev, &gnode, kUsePdl ? &pdl : nullptr, 1));
         kp.func = reinterpret_cast<void*>(k_finish);
         kp.gridDim = dim3(fin_grid);
         kp.blockDim = dim3(256);
         kp.sharedMemBytes = 0;
-        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, &gnode, 1, &kp));
+        CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&fnode, body, nullptr, 0, &kp));
+        CCDK_CUDA_CHECK(cudaGraphAddDependencies_v2(body, &gnode, &fnode, kUsePdl ? &pdl : nullptr, 1));
         prev = fnode;
     }
     CCDK_CUDA_CHECK(cudaGraphInstantiate(&G.exec, G.graph, 0));
