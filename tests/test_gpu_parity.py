@@ -589,3 +589,23 @@ def test_chunked_upload_equals_single_run(ctx):
     assert chunked.peak_queue == single.peak_queue
     assert chunked.generations == single.generations
     assert bits(np.array([chunked.global_toi]))[0] == bits(np.array([single.global_toi]))[0]
+
+
+def test_device_batch_chunking_equals_single_run(ctx):
+    """ccdk_narrow_phase_device runs very large batches as consecutive BFS
+    runs over chunks; outputs and stats (incl. the combined peak queue) must
+    equal the host API's single run on the same queries."""
+    import torch
+    qb = scenes.mixed_queries(4_300_000, seed=7, every=10000, n_exhaust=1)
+    single = ck.narrow_phase(qb, ctx=ctx)  # pageable numpy -> one run
+    k = torch.from_numpy(qb.kind).cuda()
+    p = torch.from_numpy(qb.points).cuda()
+    toi = torch.empty(len(qb), dtype=torch.float64, device="cuda")
+    fl = torch.empty(len(qb), dtype=torch.uint8, device="cuda")
+    out = ck.narrow_phase_device(k.data_ptr(), p.data_ptr(), len(qb), toi_ptr=toi.data_ptr(),
+                                 flags_ptr=fl.data_ptr(), ctx=ctx)
+    assert_bits(toi.cpu().numpy(), single.toi)
+    np.testing.assert_array_equal(fl.cpu().numpy(), single.flags)
+    assert out.total_splits == single.total_splits and out.evaluations == single.evaluations
+    assert out.peak_queue == single.peak_queue and out.generations == single.generations
+    assert out.global_toi == single.global_toi
