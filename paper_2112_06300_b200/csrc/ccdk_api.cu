@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -1341,7 +1342,8 @@ int ccdk_narrow_phase_device(ccdk_ctx* ctx, const uint8_t* kind, const double* p
         // (narrowphase.hpp:93-96) and the per-generation queue sizes are
         // summed (gen_acc), so outputs and stats equal one run.  A bounded
         // queue capacity tests the whole batch's queue and is not chunked.
-        constexpr uint64_t kMinChunk = uint64_t(1) << 21;
+        static const uint64_t kMinChunk = std::getenv("CCDK_CHUNK") ? std::strtoull(std::getenv("CCDK_CHUNK"), nullptr, 10)
+                                                                    : uint64_t(1) << 21;
         const bool chunked = n >= 2 * kMinChunk && queue_capacity == UINT64_MAX;
         const uint64_t chunk = chunked ? std::max<uint64_t>(kMinChunk, (n + 2) / 3) : n;
         const uint64_t nchunks = (n + chunk - 1) / chunk;
