@@ -417,7 +417,11 @@ def run_ours(args):
     # (SURVEY §8(d)); peak = 148 SMs x 64 fp64 lanes x clock (nominal, not in
     # MEASURED_PEAKS.json, which has only HBM and bf16)
     flops = 339.0 * d["evaluations"] + 96.0 * d["split_actions"]
-    fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
+    # fp64 peak: MEASURED dependent-free DADD throughput on this B200,
+    # 62.7 ops/SM/clk (tools/ubench_fp64.cu, profiles/r01_ubench_fp64.txt; the
+    # nominal 64 lanes x 148 SMs); MEASURED_PEAKS.json carries only HBM and bf16
+    sm_clk = clk.get("sm_mhz") or sm_max
+    fp64_peak = 148 * 62.7 * sm_clk * 1e6 / 1e12
     narrow_tf = flops / (d["ms_narrow"] * 1e-3) / 1e12 if d["ms_narrow"] > 0 else 0.0
     k = scene.primitive_count()
     sweep_bytes = 40.0 * k + 8.0 * rep.candidate_count
@@ -428,7 +432,9 @@ def run_ours(args):
                 "bound": "fp64", "achieved": narrow_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": narrow_tf / fp64_peak, "traffic": traffic.get("k_generation_bytes_per_launch"),
                 "traffic_note": traffic.get("note"),
-                "peak_source": "nominal: 148 SM x 64 fp64 FMA-pipe lanes x sm clock (non-FMA op rate)",
+                "peak_source": "measured DADD rate 62.7/SM/clk (profiles/r01_ubench_fp64.txt) x 148 SMs x "
+                               "sampled SM clock; bound is the fp64 pipe (neither HBM nor tensor cores: "
+                               "bit-exact fp64 interval arithmetic, no FMA)",
                 "algorithmic": f"F = 339*E + 96*S, E={d['evaluations']}, S={d['split_actions']}"}
     roofline_sweep = {"kernel": "run ends + tile sweep + heavy sweep", "bound": "hbm",
                       "achieved": sweep_gbs, "peak": hbm_peak, "unit": "GB/s",
