@@ -137,37 +137,46 @@ struct SplitRec {
     unsigned long long dp;
 };
 
+// The three cursor atomics are one instruction (lane d bumps region d), so
+// the warp waits for one atomic round trip per batch, not up to three.
 __device__ __forceinline__ void append_splits(const GenArgs& a, int nb, unsigned lane, unsigned q,
                                               const SplitRec r[2])
 {
     const unsigned lt = (1u << lane) - 1;
+    unsigned off[2] = {0, 0}; // slot of each child within its region's share
+    unsigned my_cnt = 0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         const unsigned m0 = __ballot_sync(0xffffffffu, r[0].dim == d);
         const unsigned m1 = __ballot_sync(0xffffffffu, r[1].dim == d);
-        const unsigned cnt = __popc(m0) + __popc(m1);
-        if (!cnt)
-            continue;
-        const int leader = __ffs(m0 | m1) - 1;
-        unsigned long long base = 0;
-        if (lane == static_cast<unsigned>(leader))
-            base = atomicAdd(&a.sc->next_pairs[d], static_cast<unsigned long long>(cnt));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        const Region& R = a.reg[nb][d];
+        if (r[0].dim == d)
+            off[0] = __popc(m0 & lt);
+        if (r[1].dim == d)
+            off[1] = __popc(m0) + __popc(m1 & lt);
+        if (lane == static_cast<unsigned>(d))
+            my_cnt = __popc(m0) + __popc(m1);
+    }
+    if (!__any_sync(0xffffffffu, my_cnt != 0))
+        return;
+    unsigned long long base = 0;
+    if (my_cnt)
+        base = atomicAdd(&a.sc->next_pairs[lane], static_cast<unsigned long long>(my_cnt));
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-            if (r[ch].dim != d)
-                continue;
-            const unsigned long long slot = base + (ch ? __popc(m0) + __popc(m1 & lt) : __popc(m0 & lt));
-            if (slot < a.cap_pairs) {
-                R.qid[slot] = q;
-                R.t[slot] = r[ch].tlo;
-                R.u[slot] = r[ch].ulo;
-                R.v[slot] = r[ch].vlo;
-                R.dep[slot] = r[ch].dp;
-            } else {
-                a.sc->phys_overflow = 1;
-            }
+    for (int ch = 0; ch < 2; ++ch) {
+        const int d = r[ch].dim;
+        const unsigned long long b = __shfl_sync(0xffffffffu, base, d < 0 ? 0 : d);
+        if (d < 0)
+            continue;
+        const unsigned long long slot = b + off[ch];
+        const Region& R = a.reg[nb][d];
+        if (slot < a.cap_pairs) {
+            R.qid[slot] = q;
+            R.t[slot] = r[ch].tlo;
+            R.u[slot] = r[ch].ulo;
+            R.v[slot] = r[ch].vlo;
+            R.dep[slot] = r[ch].dp;
+        } else {
+            a.sc->phys_overflow = 1;
         }
     }
 }
