@@ -13,6 +13,11 @@
  *   - every function returns a ccdk_status; CCDK_INVALID_INPUT maps to
  *     ccdkit::InvalidInput and CCDK_CONFIG to ccdkit::ConfigError;
  *     ccdk_last_error() returns the thread-local message of the last failure;
+ *   - calls on one context are serialised by its mutex; results a context
+ *     holds for a later fetch (candidate pairs, round sizes, per-query
+ *     results, the resident scene) belong to its last producing call, so a
+ *     caller sharing a context across threads holds its own lock around a
+ *     produce-then-fetch sequence (the C++ shim and the Python package do);
  *   - all array arguments are HOST pointers unless the name ends in _dev;
  *   - a primitive id is packed as (kind << 32) | index (kind 0 = vertex,
  *     1 = edge, 2 = face), so u64 order equals the reference's PrimitiveId

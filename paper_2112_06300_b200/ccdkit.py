@@ -216,17 +216,18 @@ def _broad(method, boxes: Boxes, scene: SceneStep, stats, rng, ctx):
     kd, ix = u8(boxes.owner_kind), u32(boxes.owner_index)
     n = C.c_uint64()
     st = abi.StqStats()
-    check(lib().ccdk_broad_phase(c.h, method, p(mn, P_F32), p(mx, P_F32), p(kd, P_U8), p(ix, P_U32),
-                                 len(boxes), scene.nv, p(scene.edges, P_U32), scene.ne,
-                                 p(scene.faces, P_U32), scene.nf, rng.begin, rng.end, C.byref(n),
-                                 C.byref(st)))
-    out = np.empty((n.value, 2), np.uint64)
-    if n.value:
-        check(lib().ccdk_fetch_pairs(c.h, p(out, P_U64)))
-    if stats is not None:
-        rounds = np.empty(st.n_rounds, np.uint64)
-        if st.n_rounds:
+    with c.lock:  # the pairs and round sizes are the context's until its next call
+        check(lib().ccdk_broad_phase(c.h, method, p(mn, P_F32), p(mx, P_F32), p(kd, P_U8), p(ix, P_U32),
+                                     len(boxes), scene.nv, p(scene.edges, P_U32), scene.ne,
+                                     p(scene.faces, P_U32), scene.nf, rng.begin, rng.end, C.byref(n),
+                                     C.byref(st)))
+        out = np.empty((n.value, 2), np.uint64)
+        if n.value:
+            check(lib().ccdk_fetch_pairs(c.h, p(out, P_U64)))
+        rounds = np.empty(st.n_rounds if stats is not None else 0, np.uint64)
+        if stats is not None and st.n_rounds:
             check(lib().ccdk_fetch_round_sizes(c.h, p(rounds, P_U64)))
+    if stats is not None:
         stats.round_sizes.extend(int(x) for x in rounds)
         stats.max_queue = max(stats.max_queue, int(st.max_queue))
         stats.pair_tests = int(st.pair_tests)
@@ -411,14 +412,15 @@ def ccd(scene: SceneStep, cfg: PipelineConfig | None = None, want_candidates: bo
         raise InvalidInput(abi.INVALID_INPUT, "vertex snapshots differ in length")
     r = abi.Report()
     ccfg = cfg.to_c()
-    check(lib().ccdk_ccd(c.h, p(scene.vertices_t0, P_F64), p(scene.vertices_t1, P_F64), scene.nv,
-                         p(scene.edges, P_U32), scene.ne, p(scene.faces, P_U32), scene.nf,
-                         C.byref(ccfg), C.byref(r)))
     pairs = None
-    if want_candidates:
-        pairs = np.empty((r.candidate_count, 2), np.uint64)
-        if r.candidate_count:
-            check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
+    with c.lock:
+        check(lib().ccdk_ccd(c.h, p(scene.vertices_t0, P_F64), p(scene.vertices_t1, P_F64), scene.nv,
+                             p(scene.edges, P_U32), scene.ne, p(scene.faces, P_U32), scene.nf,
+                             C.byref(ccfg), C.byref(r)))
+        if want_candidates:
+            pairs = np.empty((r.candidate_count, 2), np.uint64)
+            if r.candidate_count:
+                check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
     return _report(r, pairs)
 
 
@@ -428,14 +430,15 @@ def ccd_no_zero_toi(scene: SceneStep, cfg: PipelineConfig, want_candidates: bool
     c = _ctx(ctx)
     r = abi.Report()
     ccfg = cfg.to_c()
-    check(lib().ccdk_ccd_no_zero_toi(c.h, p(scene.vertices_t0, P_F64), p(scene.vertices_t1, P_F64),
-                                     scene.nv, p(scene.edges, P_U32), scene.ne, p(scene.faces, P_U32),
-                                     scene.nf, C.byref(ccfg), C.byref(r)))
     pairs = None
-    if want_candidates:
-        pairs = np.empty((r.candidate_count, 2), np.uint64)
-        if r.candidate_count:
-            check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
+    with c.lock:
+        check(lib().ccdk_ccd_no_zero_toi(c.h, p(scene.vertices_t0, P_F64), p(scene.vertices_t1, P_F64),
+                                         scene.nv, p(scene.edges, P_U32), scene.ne, p(scene.faces, P_U32),
+                                         scene.nf, C.byref(ccfg), C.byref(r)))
+        if want_candidates:
+            pairs = np.empty((r.candidate_count, 2), np.uint64)
+            if r.candidate_count:
+                check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
     return _report(r, pairs)
 
 
@@ -466,7 +469,9 @@ def segment_segment_distance(p0, p1, q0, q1, ctx=None) -> float:
 class ResidentScene:
     """A scene uploaded once; ``step()`` runs the device-resident CCD step
     (the timed unit of bench.py).  ``shard`` restricts the sweep to one of
-    ``shards`` equal-work slices of sorted left positions."""
+    ``shards`` equal-work slices of sorted left positions.  A context holds
+    one resident scene: a second ResidentScene on the same context replaces
+    the first, so give each its own Context."""
 
     def __init__(self, scene: SceneStep, ctx=None):
         self.ctx = _ctx(ctx)

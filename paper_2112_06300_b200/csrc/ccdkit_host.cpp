@@ -6,7 +6,10 @@
 // exceptions (InvalidInput / ConfigError); all compute is a ccdk_* call.
 // Scene validation and share_vertex are data-model helpers of SceneStep and
 // run on the host, as the reference's do.  One process-wide device context
-// (CCDK_DEVICE, default 0) serves all calls; the C ABI serialises them.
+// (CCDK_DEVICE, default 0) serves all calls; the C ABI serialises them, and
+// calls that produce a result and then fetch it from the context (ccd,
+// stq/bf/sap, run_batched) hold the shim's lock across both, so the API is
+// reentrant like the reference's (SURVEY §8(b) threading).
 #include "ccdkit/aabb.hpp"
 #include "ccdkit/broadphase.hpp"
 #include "ccdkit/distance.hpp"
@@ -26,6 +29,14 @@
 namespace ccdkit {
 
 namespace {
+
+// held across a produce-then-fetch sequence on the shared context
+std::recursive_mutex& sequence_mutex()
+{
+    static std::recursive_mutex m;
+    return m;
+}
+using SequenceGuard = std::lock_guard<std::recursive_mutex>;
 
 ccdk_ctx* context()
 {
@@ -125,6 +136,7 @@ std::vector<CandidatePair> fetch_pairs(uint64_t n)
 std::vector<CandidatePair> broad(int method, const std::vector<Aabb>& boxes, const SceneStep& scene,
                                  StqStats* stats, SweepRange range)
 {
+    SequenceGuard g(sequence_mutex());
     const size_t k = boxes.size();
     std::vector<float> mn(3 * k), mx(3 * k);
     std::vector<uint8_t> kind(k);
@@ -467,6 +479,7 @@ CCDKIT_EXPORT CcdReport ccd(const SceneStep& scene, const PipelineConfig& cfg)
     scene.validate();
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
+    SequenceGuard g(sequence_mutex());
     check(ccdk_ccd(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1), scene.vertices_t0.size(),
                    edata(scene), scene.edges.size(), fdata(scene), scene.faces.size(), &c, &r));
     return to_report(r, true);
@@ -486,6 +499,7 @@ CCDKIT_EXPORT ToiResult run_batched(const SceneStep& scene, const std::vector<Aa
         throw ConfigError("run_batched: boxes must equal build_boxes(scene, cfg.inflation)");
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
+    SequenceGuard g(sequence_mutex());
     check(ccdk_ccd(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1), scene.vertices_t0.size(),
                    edata(scene), scene.edges.size(), fdata(scene), scene.faces.size(), &c, &r));
     trace.broad_batches += r.broad_batches;
@@ -505,6 +519,7 @@ CCDKIT_EXPORT CcdReport ccd_no_zero_toi(const SceneStep& scene, const PipelineCo
     scene.validate();
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
+    SequenceGuard g(sequence_mutex());
     check(ccdk_ccd_no_zero_toi(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1),
                                scene.vertices_t0.size(), edata(scene), scene.edges.size(), fdata(scene),
                                scene.faces.size(), &c, &r));

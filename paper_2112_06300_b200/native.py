@@ -124,13 +124,17 @@ def check(rc: int):
 
 class Context:
     """One device context (streams and grow-only device buffers).  Calls are
-    serialised by a mutex inside the library."""
+    serialised by a mutex inside the library; ``lock`` is held by the Python
+    API across a produce-then-fetch sequence (e.g. ccd then its candidate
+    pairs), so one context can be shared by threads like the reference's
+    reentrant functions."""
 
     def __init__(self, device: int = 0):
         h = C.c_void_p()
         check(lib().ccdk_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self.lock = threading.RLock()
 
     def close(self):
         if self.h:

@@ -609,3 +609,47 @@ def test_device_batch_chunking_equals_single_run(ctx):
     assert out.total_splits == single.total_splits and out.evaluations == single.evaluations
     assert out.peak_queue == single.peak_queue and out.generations == single.generations
     assert out.global_toi == single.global_toi
+
+
+def test_concurrent_calls_share_a_context(ctx):
+    """The reference's functions are reentrant and ignore `threads` (SURVEY §8(b);
+    test_pipeline.cpp:96-106, test_narrowphase.cpp:196-211): host threads sharing one
+    context get exactly the single-threaded results, including ccd's candidate pairs,
+    which are fetched from the context after the step."""
+    import threading
+    qb = scenes.random_queries(600, seed=77)
+    s1 = scenes.make_cloth_scene(16, 16, 0.02, 1.0, 3)
+    s2 = scenes.make_box_soup(12, 3.0, 0.4, 1.0, 9)
+    pcfg = PipelineConfig(inflation=0.01)
+    exp_n = ck.narrow_phase(qb, NarrowConfig(), ctx=ctx)
+    exp_c = {0: ck.ccd(s1, pcfg, ctx=ctx), 1: ck.ccd(s2, pcfg, ctx=ctx)}
+    boxes = ck.build_boxes(s2, 0.01, ctx=ctx)
+    exp_b = ck.stq(boxes, s2, ctx=ctx)
+    errors, checked = [], []
+
+    def work(i):
+        try:
+            for it in range(4):
+                if (i + it) % 3 == 0:
+                    got = ck.narrow_phase(qb, NarrowConfig(), threads=1 + 7 * (i % 2), ctx=ctx)
+                    assert bits(got.toi).tolist() == bits(exp_n.toi).tolist()
+                    assert got.flags.tolist() == exp_n.flags.tolist()
+                    assert got.total_splits == exp_n.total_splits and got.peak_queue == exp_n.peak_queue
+                elif (i + it) % 3 == 1:
+                    k = (i + it) % 2
+                    got = ck.ccd(s1 if k == 0 else s2, pcfg, ctx=ctx)
+                    np.testing.assert_array_equal(got.candidates, exp_c[k].candidates)
+                    assert bits(np.array([got.toi.toi]))[0] == bits(np.array([exp_c[k].toi.toi]))[0]
+                else:
+                    np.testing.assert_array_equal(ck.stq(boxes, s2, threads=4, ctx=ctx), exp_b)
+                checked.append(1)
+        except Exception as e:  # noqa: BLE001 - surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[0]
+    assert len(checked) == 16
