@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <exception>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "ccdkit/aabb.hpp"
 #include "ccdkit/broadphase.hpp"
@@ -156,6 +158,80 @@ static void pipeline()
     CHECK(t.toi == r.toi.toi && trace.narrow_batches == 1);
 }
 
+// A grid of n x n vertices falling through z = 0 with a slight tilt.
+static SceneStep grid_scene(int n, double tilt)
+{
+    SceneStep s;
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) {
+            s.vertices_t0.push_back({ double(i), double(j), 1.0 + tilt * i });
+            s.vertices_t1.push_back({ double(i) + 0.1, double(j), -1.0 + tilt * j });
+        }
+    for (int j = 0; j + 1 < n; ++j)
+        for (int i = 0; i + 1 < n; ++i) {
+            const uint32_t a = j * n + i, b = a + 1, c = a + n, d = c + 1;
+            s.faces.push_back({ a, b, d });
+            s.faces.push_back({ a, d, c });
+            s.edges.push_back({ a, b });
+            s.edges.push_back({ a, c });
+            s.edges.push_back({ a, d });
+        }
+    for (int j = 0; j + 1 < n; ++j)
+        s.edges.push_back({ uint32_t(j * n + n - 1), uint32_t((j + 1) * n + n - 1) });
+    for (int i = 0; i + 1 < n; ++i)
+        s.edges.push_back({ uint32_t((n - 1) * n + i), uint32_t((n - 1) * n + i + 1) });
+    // a static floor triangle under the grid
+    const uint32_t f = uint32_t(s.vertices_t0.size());
+    for (const Vec3& v : { Vec3 { -1, -1, 0 }, Vec3 { 3.0 * n, -1, 0 }, Vec3 { -1, 3.0 * n, 0 } }) {
+        s.vertices_t0.push_back(v);
+        s.vertices_t1.push_back(v);
+    }
+    s.faces.push_back({ f, f + 1, f + 2 });
+    s.edges.push_back({ f, f + 1 });
+    s.edges.push_back({ f, f + 2 });
+    s.edges.push_back({ f + 1, f + 2 });
+    return s;
+}
+
+// Reentrancy (test_pipeline.cpp:96-106, test_narrowphase.cpp:196-211): calls
+// from several threads, with any `threads` value, return the single-threaded
+// results, candidate lists included.
+static void determinism_across_threads()
+{
+    const SceneStep a = grid_scene(12, 0.01), b = grid_scene(9, -0.02);
+    const CcdReport ra = ccd(a, PipelineConfig {}), rb = ccd(b, PipelineConfig {});
+    CHECK(!ra.candidates.empty() && ra.candidates.size() != rb.candidates.size());
+    const auto boxes = build_boxes(b);
+    const auto pairs = stq(boxes, b);
+    const auto q = classify(pairs, b);
+    const NarrowOutcome nb = narrow_phase(q.vertex_face, NarrowConfig {});
+    std::vector<int> bad(4, 0);
+    std::vector<std::thread> ts;
+    for (int t = 0; t < 4; ++t)
+        ts.emplace_back([&, t] {
+            for (int it = 0; it < 6; ++it) {
+                const int k = (t + it) % 3;
+                if (k == 0) {
+                    const CcdReport r = ccd(t % 2 ? b : a, PipelineConfig {});
+                    const CcdReport& e = t % 2 ? rb : ra;
+                    bad[t] += !(r.candidates == e.candidates && r.toi.toi == e.toi.toi);
+                } else if (k == 1) {
+                    bad[t] += !(stq(boxes, b, 1 + 7 * (t % 2)) == pairs);
+                } else {
+                    const NarrowOutcome o = narrow_phase(q.vertex_face, NarrowConfig {}, 8);
+                    bool same = o.total_splits == nb.total_splits && o.per_query.size() == nb.per_query.size();
+                    for (size_t i = 0; same && i < o.per_query.size(); ++i)
+                        same = o.per_query[i].toi == nb.per_query[i].toi;
+                    bad[t] += !same;
+                }
+            }
+        });
+    for (auto& th : ts)
+        th.join();
+    for (int t = 0; t < 4; ++t)
+        CHECK(bad[t] == 0);
+}
+
 int main()
 {
     try {
@@ -163,6 +239,7 @@ int main()
         broadphase();
         narrowphase();
         pipeline();
+        determinism_across_threads();
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         return 2;

@@ -13,7 +13,7 @@ SRC = os.path.join(ROOT, "tests", "cpp", "test_ccdkit_api.cpp")
 
 def _compile(tmp_path):
     exe = str(tmp_path / "test_ccdkit_api")
-    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), SRC, "-o", exe,
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-pthread", "-I", os.path.join(ROOT, "include"), SRC, "-o", exe,
                         "-L", LIB, "-lccdkit", "-lccdk", f"-Wl,-rpath,{LIB}"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     return exe
