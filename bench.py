@@ -243,10 +243,14 @@ def narrow_only_leg(args, torch, ck, scenes, stream, flush, rank, world, local):
         e2e_ms = None
         if not args.no_e2e:
             hq = scenes.QueryBatch(kind_h.numpy(), pts_h.numpy())
-            ck.narrow_phase(hq)  # warm-up: device buffers sized outside the timed call
+            # per-query results land in pinned host buffers (the C ABI's
+            # caller-provided outputs), allocated outside the timed call
+            toi_h = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+            flags_h = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
+            ck.narrow_phase(hq, toi_out=toi_h, flags_out=flags_h)  # warm-up: device buffers sized
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            res = ck.narrow_phase(hq)
+            res = ck.narrow_phase(hq, toi_out=toi_h, flags_out=flags_h)
             b.record(stream)
             torch.cuda.synchronize()
             e2e_ms = a.elapsed_time(b)

@@ -349,10 +349,21 @@ def split_box(box, depth, d: int):
     return left, dl, right, dl.copy()
 
 
+def _out_array(a, n: int, dtype, name: str) -> np.ndarray:
+    if a is None:
+        return np.empty(max(n, 1), dtype)
+    if a.dtype != dtype or a.ndim != 1 or a.shape[0] < n or not a.flags.c_contiguous or not a.flags.writeable:
+        raise ConfigError(abi.CONFIG, f"narrow_phase: {name} must be a writable contiguous {np.dtype(dtype)}[{n}]")
+    return a if n else np.empty(1, dtype)
+
+
 def narrow_phase(queries: QueryBatch, cfg: NarrowConfig | None = None, threads: int = 1,
                  queue_capacity: int = abi.UINT64_MAX, per_query_min_sep=None,
-                 ctx=None) -> NarrowOutcome:
-    """narrow_phase (narrowphase.hpp:97-100)."""
+                 ctx=None, toi_out=None, flags_out=None) -> NarrowOutcome:
+    """narrow_phase (narrowphase.hpp:97-100).  ``toi_out`` / ``flags_out``
+    (float64[n] / uint8[n], C-contiguous; e.g. views of pinned host memory)
+    receive the per-query results in place, as the C ABI's caller-provided
+    output buffers do; by default fresh arrays are returned."""
     cfg = cfg or NarrowConfig()
     c = _ctx(ctx)
     n = len(queries)
@@ -361,13 +372,13 @@ def narrow_phase(queries: QueryBatch, cfg: NarrowConfig | None = None, threads: 
     kind = u8(queries.kind)
     pts = f64(queries.points).reshape(-1, 24)
     seps = None if per_query_min_sep is None else f64(per_query_min_sep)
-    toi = np.empty(max(n, 1), np.float64)
-    flags = np.empty(max(n, 1), np.uint8)
+    toi = _out_array(toi_out, n, np.float64, "toi_out")
+    flags = _out_array(flags_out, n, np.uint8, "flags_out")
     st = abi.NarrowStats()
     ccfg = cfg.to_c()
     check(lib().ccdk_narrow_phase(c.h, p(kind, P_U8), p(pts, P_F64), p(seps, P_F64), n, C.byref(ccfg),
                                   queue_capacity, p(toi, P_F64), p(flags, P_U8), C.byref(st)))
-    return NarrowOutcome(toi[:n].copy(), flags[:n].copy(), st.global_toi, bool(st.overflow),
+    return NarrowOutcome(toi[:n], flags[:n], st.global_toi, bool(st.overflow),
                          int(st.peak_queue), int(st.total_splits), int(st.evaluations),
                          int(st.split_actions), int(st.generations), float(st.device_ms))
 

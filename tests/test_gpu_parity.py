@@ -653,3 +653,22 @@ def test_concurrent_calls_share_a_context(ctx):
         t.join()
     assert not errors, errors[0]
     assert len(checked) == 16
+
+
+def test_narrow_phase_caller_output_buffers(ctx):
+    """Per-query results into caller-provided (here pinned) host buffers, like the C ABI's
+    output pointers: identical to the returned arrays; wrong buffers are a ConfigError."""
+    import torch
+    qb = scenes.random_queries(2000, seed=91)
+    exp = ck.narrow_phase(qb, ctx=ctx)
+    toi_h = torch.full((2000,), -1.0, dtype=torch.float64).pin_memory().numpy()
+    fl_h = torch.full((2000,), 255, dtype=torch.uint8).pin_memory().numpy()
+    got = ck.narrow_phase(qb, ctx=ctx, toi_out=toi_h, flags_out=fl_h)
+    assert np.shares_memory(got.toi, toi_h) and np.shares_memory(got.flags, fl_h)
+    assert_bits(toi_h, exp.toi)
+    np.testing.assert_array_equal(fl_h, exp.flags)
+    assert got.total_splits == exp.total_splits and got.peak_queue == exp.peak_queue
+    with pytest.raises(ck.ConfigError):
+        ck.narrow_phase(qb, ctx=ctx, toi_out=np.empty(2000, np.float32))
+    with pytest.raises(ck.ConfigError):
+        ck.narrow_phase(qb, ctx=ctx, flags_out=np.empty(10, np.uint8))

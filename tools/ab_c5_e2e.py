@@ -11,11 +11,14 @@ pt = torch.from_numpy(qb.points).pin_memory()
 hq = scenes.QueryBatch(kt.numpy(), pt.numpy())
 ck.narrow_phase(hq)
 torch.cuda.synchronize()
-for _ in range(2):
+toi_h = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+fl_h = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
+for pinned in (False, True, False, True):
+    kw = dict(toi_out=toi_h, flags_out=fl_h) if pinned else {}
     t0 = time.perf_counter()
-    out = ck.narrow_phase(hq)
+    out = ck.narrow_phase(hq, **kw)
     t1 = time.perf_counter()
-    print(f"e2e wall {1e3 * (t1 - t0):.1f} ms, narrow device (sum of chunks) {out.device_ms:.1f} ms")
+    print(f"e2e wall {1e3 * (t1 - t0):.1f} ms (pinned outputs {pinned}), narrow device (sum of chunks) {out.device_ms:.1f} ms")
 d = torch.empty(pt.shape, dtype=pt.dtype, device="cuda")
 torch.cuda.synchronize()
 t0 = time.perf_counter()
