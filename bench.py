@@ -238,7 +238,8 @@ def narrow_only_leg(args, torch, ck, scenes, stream, flush, rank, world, local):
             b.record(stream)
             evs.append((a, b))
         torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        ms = sum(step_ms) / len(step_ms)
         # e2e: host queries -> C ABI -> host per-query results
         e2e_ms = None
         if not args.no_e2e:
@@ -265,6 +266,8 @@ def narrow_only_leg(args, torch, ck, scenes, stream, flush, rank, world, local):
            "ms": ms, "queries_per_s": n_all / (ms * 1e-3),
            "global_toi": float(gtoi.item()), "evaluations": evals, "split_actions": splits,
            "total_splits": total_splits, "generations_rank0": out.generations,
+           "ms_steps_rank0": [round(x, 3) for x in step_ms],
+           "ms_device_runs_rank0": round(out.device_ms, 3),
            "sharding": f"contiguous query blocks x{world}, allreduce(min)",
            "e2e": None if e2e_ms is None else {
                "value": n_all / (e2e_ms * 1e-3), "unit": "queries/s", "ms": e2e_ms,

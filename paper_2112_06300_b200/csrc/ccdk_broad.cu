@@ -436,7 +436,7 @@ __device__ __forceinline__ bool bf_ok(const SweepArgs& a, unsigned long long p, 
 #define CCDK_SWEEP_RPW 8
 #endif
 #ifndef CCDK_SWEEP_TB
-#define CCDK_SWEEP_TB 1024
+#define CCDK_SWEEP_TB 512
 #endif
 constexpr int kRowsPerWarp = CCDK_SWEEP_RPW;
 constexpr int kRowsTB = CCDK_SWEEP_TB;
@@ -542,7 +542,10 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
         drain_hits(a, p, mb, mv, hits, nh, lane, true);
 }
 
-__global__ void __launch_bounds__(kRowsTB) k_sweep_rows(SweepArgs a)
+#ifndef CCDK_SWEEP_MINB
+#define CCDK_SWEEP_MINB 3
+#endif
+__global__ void __launch_bounds__(kRowsTB, CCDK_SWEEP_MINB) k_sweep_rows(SweepArgs a)
 {
     __shared__ unsigned s_hits[kRowsTB / 32][kHitBuf];
     const unsigned lane = threadIdx.x & 31;
