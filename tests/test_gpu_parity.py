@@ -589,6 +589,12 @@ def test_chunked_upload_equals_single_run(ctx):
     assert chunked.peak_queue == single.peak_queue
     assert chunked.generations == single.generations
     assert bits(np.array([chunked.global_toi]))[0] == bits(np.array([single.global_toi]))[0]
+    # the bench's end-to-end form: pinned inputs and pinned caller-provided outputs
+    toi_h = torch.empty(len(qb), dtype=torch.float64).pin_memory().numpy()
+    fl_h = torch.empty(len(qb), dtype=torch.uint8).pin_memory().numpy()
+    ck.narrow_phase(scenes.QueryBatch(kt.numpy(), pt.numpy()), ctx=ctx, toi_out=toi_h, flags_out=fl_h)
+    assert_bits(toi_h, single.toi)
+    np.testing.assert_array_equal(fl_h, single.flags)
 
 
 def test_device_batch_chunking_equals_single_run(ctx):
