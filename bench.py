@@ -199,6 +199,58 @@ def run_reference(args):
     return 0
 
 
+def candidate_fingerprint(pairs):
+    """FNV-1a over the (left, right) packed ids in order, as libccdkit_bench computes it."""
+    x = 1469598103934665603
+    m = (1 << 64) - 1
+    for v in pairs.reshape(-1).tolist():
+        x = ((x ^ v) * 1099511628211) & m
+    return x
+
+
+def dropin_e2e(args, torch, scene, flush, resident_fp, rep):
+    """The reference's own entry point through the drop-in library: one
+    ccdkit::ccd(SceneStep, PipelineConfig) call per step (libccdkit.so over the
+    C ABI), scene in pageable std::vectors (H2D inside), CcdReport returned by
+    value with all candidate pairs (D2H + container fill inside).  Host wall
+    time of the synchronous call; L2 flushed before each call."""
+    import ctypes as C
+    import numpy as np
+    lib = C.CDLL(os.path.join(ROOT, "paper_2112_06300_b200", "lib", "libccdkit_bench.so"))
+    lib.ccdkit_bench_prepare.restype = C.c_void_p
+    lib.ccdkit_bench_prepare.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                         C.c_void_p, C.c_uint64, C.c_double]
+    lib.ccdkit_bench_run.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    lib.ccdkit_bench_free.argtypes = [C.c_void_p]
+    lib.ccdkit_bench_last_error.restype = C.c_char_p
+    arrs = [np.ascontiguousarray(a) for a in (scene.vertices_t0, scene.vertices_t1, scene.edges, scene.faces)]
+    h = lib.ccdkit_bench_prepare(arrs[0].ctypes.data, arrs[1].ctypes.data, scene.nv, arrs[2].ctypes.data,
+                                 scene.ne, arrs[3].ctypes.data, scene.nf, 0.01)
+    ms, ncand, toi, fp = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
+    times = []
+    try:
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if lib.ccdkit_bench_run(h, C.byref(ms), C.byref(ncand), C.byref(toi), C.byref(fp)) != 0:
+                raise RuntimeError(lib.ccdkit_bench_last_error().decode())
+            if i >= args.warmup:
+                times.append(ms.value)
+    finally:
+        lib.ccdkit_bench_free(h)
+    e2e = sum(times) / len(times)
+    return {"value": e2e, "unit": "ms", "h2d_bytes_per_step": int(scene.nbytes),
+            "d2h_bytes_per_step": int(16 * ncand.value + C_REPORT_BYTES),
+            "api": "ccdkit::ccd(const SceneStep&, const PipelineConfig&) -> CcdReport (libccdkit.so, "
+                   "include/ccdkit/pipeline.hpp), pageable host vectors in, all candidates out",
+            "timer": "host wall clock around the synchronous call, L2 flushed before each",
+            "candidates": int(ncand.value), "toi": toi.value,
+            "matches_device_resident_run": bool(ncand.value == rep.candidate_count and toi.value == rep.toi.toi
+                                                and (resident_fp is None or fp.value == resident_fp)),
+            "steps_ms": [round(t, 3) for t in times]}
+
+
 def narrow_only_leg(args, torch, ck, scenes, stream, flush, rank, world, local):
     """BASELINE config 5: narrow phase only over 10M mixed VF/EE queries incl.
     rotated near-degenerates and 16 budget-exhausting slides.  Queries are
@@ -351,7 +403,7 @@ def run_ours(args):
         rep = reps[-1]
         gtoi = sharded.global_toi(rep)
 
-        # ---- e2e through the C ABI from pinned host buffers
+        # ---- e2e through the resident multi-GPU API from pinned host buffers
         e2e_ms = None
         h2d = scene.nbytes
         d2h = C_REPORT_BYTES + 8
@@ -379,6 +431,15 @@ def run_ours(args):
                     e2e_ev.append((a, b))
             torch.cuda.synchronize()
             e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev) / len(e2e_ev)
+        resident_fp = None
+        if world == 1:
+            resident_fp = candidate_fingerprint(resident.candidates(rep.candidate_count))
+
+    # ---- e2e through the drop-in: ccdkit::ccd (libccdkit.so) from pageable
+    # SceneStep vectors, CcdReport with every candidate pair (pipeline.cpp:218-232)
+    dropin = None
+    if world == 1 and not args.no_e2e:
+        dropin = dropin_e2e(args, torch, scene, flush, resident_fp, rep)
 
     # ---- max over ranks
     vals = torch.tensor([my_ms, e2e_ms or 0.0, rep.device["ms_narrow"]], dtype=torch.float64,
@@ -474,8 +535,14 @@ def run_ours(args):
         "work": {"pair_tests": d["pair_tests"], "evaluations": d["evaluations"],
                  "split_actions": d["split_actions"], "total_splits": d["total_splits"],
                  "generations": d["generations"], "peak_queue": d["peak_queue"]},
-        "e2e": {"value": e2e_max if e2e_ms is not None else None, "unit": "ms",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": dropin if dropin is not None else
+               {"value": e2e_max if e2e_ms is not None else None, "unit": "ms",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "multigpu.RebalancedCcd/ShardedCcd over ResidentScene (pinned host scene in, ToI out)"},
+        "e2e_resident": {"value": e2e_max if e2e_ms is not None else None, "unit": "ms",
+                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                         "api": "ResidentScene upload (pinned host buffers) + ccdk_ccd_resident step + "
+                                "global ToI; candidates stay on the device"},
         "roofline": roofline, "roofline_sweep": roofline_sweep,
         "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": int(d["kernel_launches"]) * args.steps,

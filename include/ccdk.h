@@ -110,6 +110,8 @@ typedef struct {
     uint64_t n_rounds;       /* length of round_sizes; fetch with ccdk_fetch_round_sizes */
     uint64_t pair_tests;     /* sum of run lengths over the left range (roofline T) */
     uint64_t axis;
+    uint64_t axis_flags;     /* bit0: tree variances within the error bound of a tie,
+                                bit1: axis decided by the reference's serial sums */
 } ccdk_stq_stats;
 
 /* CcdReport (pipeline.hpp:47-61); stage times in seconds like the reference. */

@@ -36,7 +36,8 @@ class NarrowStats(C.Structure):
 
 class StqStats(C.Structure):
     _fields_ = [("max_queue", C.c_uint64), ("n_rounds", C.c_uint64),
-                ("pair_tests", C.c_uint64), ("axis", C.c_uint64)]
+                ("pair_tests", C.c_uint64), ("axis", C.c_uint64),
+                ("axis_flags", C.c_uint64)]
 
 
 class Report(C.Structure):

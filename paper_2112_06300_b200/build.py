@@ -3,6 +3,8 @@
     libccdk.so    CUDA kernels + the C ABI (include/ccdk.h)
     libccdkit.so  C++ host API with the reference signatures
                   (include/ccdkit/*.hpp) layered on libccdk.so
+    libccdkit_bench.so  end-to-end timing harness: ccdkit::ccd through
+                  libccdkit.so from pageable host vectors (bench.py e2e)
 
 Both land in paper_2112_06300_b200/lib/ so they travel with the repository
 snapshot to the GPU box.  Flags: no FMA contraction (--fmad=false, and the
@@ -74,6 +76,12 @@ def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False) 
     if os.path.exists(cxx) and (force or _stale(so2, [cxx, so] + ccdkit_headers)):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, cxx, "-o", so2,
               "-L", LIB, "-lccdk", "-Wl,-rpath,$ORIGIN"], verbose)
+    # end-to-end timing harness over the drop-in (bench.py's e2e leg)
+    hb = os.path.join(CSRC, "ccdkit_bench.cpp")
+    so3 = os.path.join(LIB, "libccdkit_bench.so")
+    if os.path.exists(hb) and (force or _stale(so3, [hb, so2] + ccdkit_headers)):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, hb, "-o", so3,
+              "-L", LIB, "-lccdkit", "-Wl,-rpath,$ORIGIN"], verbose)
     return so
 
 

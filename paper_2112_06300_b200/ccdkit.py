@@ -69,6 +69,7 @@ class StqStats:
     round_sizes: list = field(default_factory=list)
     pair_tests: int = 0
     axis: int = 0
+    axis_flags: int = 0  # bit0 near tie under the tree sums, bit1 serial order decided
 
 
 @dataclass
@@ -232,6 +233,7 @@ def _broad(method, boxes: Boxes, scene: SceneStep, stats, rng, ctx):
         stats.max_queue = max(stats.max_queue, int(st.max_queue))
         stats.pair_tests = int(st.pair_tests)
         stats.axis = int(st.axis)
+        stats.axis_flags = int(st.axis_flags)
     return out
 
 
@@ -481,17 +483,27 @@ class ResidentScene:
     """A scene uploaded once; ``step()`` runs the device-resident CCD step
     (the timed unit of bench.py).  ``shard`` restricts the sweep to one of
     ``shards`` equal-work slices of sorted left positions.  A context holds
-    one resident scene: a second ResidentScene on the same context replaces
-    the first, so give each its own Context."""
+    one resident scene (in its own slot: per-call uploads of ccd, build_boxes,
+    classify never touch it); a second ResidentScene on the same context
+    replaces the first, and the first then raises ConfigError on use, so give
+    each its own Context."""
 
     def __init__(self, scene: SceneStep, ctx=None):
+        import weakref
         self.ctx = _ctx(ctx)
         self.scene = scene
         check(lib().ccdk_scene_upload(self.ctx.h, p(scene.vertices_t0, P_F64),
                                       p(scene.vertices_t1, P_F64), scene.nv, p(scene.edges, P_U32),
                                       scene.ne, p(scene.faces, P_U32), scene.nf))
+        self.ctx.resident_owner = weakref.ref(self)
+
+    def _check_current(self):
+        owner = getattr(self.ctx, "resident_owner", None)
+        if owner is None or owner() is not self:
+            raise ConfigError(abi.CONFIG, "ResidentScene: a later ResidentScene replaced this scene on its context")
 
     def step(self, cfg: PipelineConfig, shard: int = 0, shards: int = 1) -> CcdReport:
+        self._check_current()
         r = abi.Report()
         ccfg = cfg.to_c()
         check(lib().ccdk_ccd_resident(self.ctx.h, C.byref(ccfg), shard, shards, C.byref(r)))
@@ -500,6 +512,7 @@ class ResidentScene:
     def broad(self, cfg: PipelineConfig, shard: int = 0, shards: int = 1):
         """Box build + this shard's sweep + pair sort; keys stay on the device.
         Returns (n_pairs, key_bits, device_ms)."""
+        self._check_current()
         n, nb, ms = C.c_uint64(), C.c_int(), C.c_float()
         ccfg = cfg.to_c()
         check(lib().ccdk_broad_resident(self.ctx.h, C.byref(ccfg), shard, shards, C.byref(n), C.byref(nb),
@@ -512,6 +525,7 @@ class ResidentScene:
 
     def narrow_keys(self, cfg: PipelineConfig, keys_ptr: int, n: int, key_bits: int) -> CcdReport:
         """Classify + narrow phase on n canonical pair keys in device memory."""
+        self._check_current()
         r = abi.Report()
         ccfg = cfg.to_c()
         check(lib().ccdk_ccd_keys_resident(self.ctx.h, C.byref(ccfg), C.c_void_p(keys_ptr), n, key_bits,

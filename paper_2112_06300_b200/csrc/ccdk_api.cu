@@ -84,6 +84,9 @@ const char* scene_error_text(unsigned long long code)
     return "invalid scene";
 }
 
+// The reference throws at the FIRST failing element in its loop order (every
+// vertex, then every edge — range before distinctness — then every face), so
+// the error key is (element position << 3 | code) and the minimum wins.
 __global__ void k_validate_scene(const double* v0, const double* v1, unsigned long long nv,
                                  const uint32_t* e, unsigned long long ne, const uint32_t* f,
                                  unsigned long long nf, unsigned long long* err)
@@ -91,12 +94,14 @@ __global__ void k_validate_scene(const double* v0, const double* v1, unsigned lo
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
     for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
          i < 3 * nv + ne + nf; i += stride) {
-        unsigned long long code = kErrNone;
+        unsigned long long code = kErrNone, pos = 0;
         if (i < 3 * nv) {
+            pos = i / 3; // vertex i/3, coordinate i%3 of both snapshots
             if (!isfinite(v0[i]) || !isfinite(v1[i]))
                 code = kErrNonFinite;
         } else if (i < 3 * nv + ne) {
             const unsigned long long j = i - 3 * nv;
+            pos = nv + j;
             const uint32_t a = e[2 * j], b = e[2 * j + 1];
             if (a >= nv || b >= nv)
                 code = kErrEdgeRange;
@@ -104,6 +109,7 @@ __global__ void k_validate_scene(const double* v0, const double* v1, unsigned lo
                 code = kErrEdgeSame;
         } else {
             const unsigned long long j = i - 3 * nv - ne;
+            pos = nv + ne + j;
             const uint32_t a = f[3 * j], b = f[3 * j + 1], d = f[3 * j + 2];
             if (a >= nv || b >= nv || d >= nv)
                 code = kErrFaceRange;
@@ -111,7 +117,7 @@ __global__ void k_validate_scene(const double* v0, const double* v1, unsigned lo
                 code = kErrFaceSame;
         }
         if (code != kErrNone)
-            atomicMin(err, code);
+            atomicMin(err, (pos << 3) | code);
     }
 }
 
@@ -328,9 +334,8 @@ void validate_pipeline_cfg(const ccdk_pipeline_cfg& p)
         throw Error(CCDK_CONFIG, "PipelineConfig: inflation must be >= 0");
 }
 
-void validate_scene_dev(Ctx& c)
+void validate_scene_dev(Ctx& c, DevScene& s)
 {
-    DevScene& s = c.scene;
     auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
     CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->misc[3], 0xff, 8, c.stream));
     const uint64_t n = 3 * s.nv + s.ne + s.nf;
@@ -349,15 +354,15 @@ void check_scene_error(Ctx& c)
     d2h(c, &code, &ctr->misc[3], 8);
     sync(c);
     if (code != kErrNone)
-        throw Error(CCDK_INVALID_INPUT, scene_error_text(code));
+        throw Error(CCDK_INVALID_INPUT, scene_error_text(code & 7));
 }
 
-// Upload a scene into ctx.scene and validate it on the device
-// (SceneStep::validate, scene.cpp:13-34) before any kernel indexes it.
-void upload_scene(Ctx& c, const double* v0, const double* v1, uint64_t nv, const uint32_t* e,
+// Upload a scene into a context slot (per-call scratch or the resident
+// scene) and validate it on the device (SceneStep::validate,
+// scene.cpp:13-34) before any kernel indexes it.
+void upload_scene(Ctx& c, DevScene& s, const double* v0, const double* v1, uint64_t nv, const uint32_t* e,
                   uint64_t ne, const uint32_t* f, uint64_t nf)
 {
-    DevScene& s = c.scene;
     s.valid = false;
     s.nv = nv;
     s.ne = ne;
@@ -366,7 +371,7 @@ void upload_scene(Ctx& c, const double* v0, const double* v1, uint64_t nv, const
     h2d(c, s.v1.ensure(nv * 24), v1, nv * 24);
     h2d(c, s.edges.ensure(ne * 8), e, ne * 8);
     h2d(c, s.faces.ensure(nf * 12), f, nf * 12);
-    validate_scene_dev(c);
+    validate_scene_dev(c, s);
     check_scene_error(c);
     s.valid = true;
 }
@@ -407,9 +412,11 @@ struct BatchRun {
         bi.range_end = end;
         bi.shard_rank = shard_rank;
         bi.shard_count = shard_count;
+        // the axis matters only if the budget can force range halving
+        bi.exact_axis = cap_pairs < k * (k - 1) / 2;
         BroadOut bo;
         broad_phase(c, bi, bo);
-        launches += 11;
+        launches += bi.exact_axis ? 12 : 11;
         pair_tests += bo.pair_tests;
         ms_sort += bo.ms_axis_sort;
         ms_sweep += bo.ms_sweep;
@@ -535,11 +542,10 @@ struct BatchRun {
 
 // The full CCD step on ctx.scene (pipeline.cpp:218-232 via run_batched at the
 // default budget): build -> STQ -> classify -> narrow -> global min.
-void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_t shard_count,
+void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_t shard_count,
               ccdk_report& rep, cudaEvent_t start_event)
 {
     validate_pipeline_cfg(cfg);
-    DevScene& s = c.scene;
     std::memset(&rep, 0, sizeof rep);
     rep.toi = INFINITY;
     rep.batch_count = 1;
@@ -590,6 +596,8 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
     c.last_keys_all = true;
     c.last_pairs_general = false;
     c.last_n_pairs = run.candidates;
+    c.last_nv = s.nv;
+    c.last_ne = s.ne;
     c.last_query_count = run.queries;
     double* dtoi = grow<double>(c.last_toi, 1);
     const double toi = __builtin_bit_cast(double, static_cast<uint64_t>(run.toi_bits));
@@ -635,7 +643,7 @@ void ccd_step(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_
 // K1 on the resident scene (the scene was validated when it was uploaded).
 void build_resident_boxes(Ctx& c, const ccdk_pipeline_cfg& cfg, float*& bmin, float*& bmax, uint4*& vids)
 {
-    DevScene& s = c.scene;
+    DevScene& s = c.resident;
     const uint64_t k = s.nv + s.ne + s.nf;
     bmin = grow<float>(c.bmin, 3 * std::max<uint64_t>(k, 1));
     bmax = grow<float>(c.bmax, 3 * std::max<uint64_t>(k, 1));
@@ -658,7 +666,7 @@ void broad_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, u
                     uint64_t& n_pairs, int& key_bits, float& ms)
 {
     validate_pipeline_cfg(cfg);
-    DevScene& s = c.scene;
+    DevScene& s = c.resident;
     const uint64_t k = s.nv + s.ne + s.nf;
     cudaEvent_t e0 = c.events.get(EventPool::kStep), e1 = c.events.get(EventPool::kStep + 1);
     CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
@@ -676,12 +684,17 @@ void broad_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, u
         bi.method = CCDK_BROAD_STQ;
         bi.shard_rank = shard_rank;
         bi.shard_count = shard_count;
+        bi.exact_axis = false; // the shards' union is the full set for any common axis
         BroadOut bo;
         broad_phase(c, bi, bo);
         n_pairs = bo.n_pairs;
         key_bits = c.last_nb;
     }
     c.last_n_pairs = n_pairs;
+    c.last_keys_all = false;
+    c.last_pairs_general = false;
+    c.last_nv = s.nv;
+    c.last_ne = s.ne;
     CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
     CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
@@ -693,7 +706,7 @@ void ccd_keys_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, const uint64_t* key
                        int key_bits, ccdk_report& rep)
 {
     validate_pipeline_cfg(cfg);
-    DevScene& s = c.scene;
+    DevScene& s = c.resident;
     const uint64_t k = s.nv + s.ne + s.nf;
     if (key_bits != ceil_log2(std::max<uint64_t>(k, 2)))
         throw Error(CCDK_CONFIG, "ccdk_ccd_keys_resident: key width does not match the resident scene");
@@ -716,6 +729,8 @@ void ccd_keys_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, const uint64_t* key
     c.last_keys_all = true;
     c.last_pairs_general = false;
     c.last_n_pairs = run.candidates;
+    c.last_nv = s.nv;
+    c.last_ne = s.ne;
     c.last_query_count = run.queries;
     const double toi = __builtin_bit_cast(double, static_cast<uint64_t>(run.toi_bits));
     double* dtoi = grow<double>(c.last_toi, 1);
@@ -849,7 +864,7 @@ int ccdk_build_boxes(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t
         std::lock_guard<std::mutex> lk(ctx->mu);
         Ctx& c = *ctx;
         CCDK_CUDA_CHECK(cudaSetDevice(c.device));
-        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
+        upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
         if (inflation < 0.0)
             throw Error(CCDK_INVALID_INPUT, "build_boxes: inflation must be >= 0");
         const uint64_t k = nv + ne + nf;
@@ -993,6 +1008,10 @@ int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner, const f
         bi.range_begin = range_begin;
         bi.range_end = range_end;
         bi.want_rounds = stats != nullptr && method == CCDK_BROAD_STQ;
+        // the axis is observable through StqStats, partial SweepRanges and
+        // the reported axis; a full-range pair list does not depend on it
+        bi.exact_axis = method != CCDK_BROAD_BF
+            && (stats != nullptr || range_begin > 0 || range_end < k - 1);
         bi.unique = nranks < k;
         BroadOut bo;
         broad_phase(c, bi, bo);
@@ -1003,6 +1022,7 @@ int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner, const f
             stats->max_queue = c.last_rounds.empty() ? 0 : c.last_rounds[0];
             stats->pair_tests = bo.pair_tests;
             stats->axis = static_cast<uint64_t>(bo.axis);
+            stats->axis_flags = (bo.axis_near_tie ? 1u : 0u) | (bo.axis_serial ? 2u : 0u);
         }
     });
 }
@@ -1021,7 +1041,7 @@ int ccdk_fetch_pairs(ccdk_ctx* ctx, uint64_t* out)
         launch_keys_to_ids(c, keys, n, c.last_nb,
                            c.last_pairs_general ? c.own_kind.as<uint8_t>() : nullptr,
                            c.last_pairs_general ? c.own_index.as<uint32_t>() : nullptr,
-                           c.scene.nv, c.scene.ne, ids);
+                           c.last_nv, c.last_ne, ids);
         d2h(c, out, ids, 16 * n);
         sync(c);
     });
@@ -1047,7 +1067,7 @@ int ccdk_classify(ccdk_ctx* ctx, const uint64_t* pairs, uint64_t n_pairs, const 
         if (!n_pairs)
             return;
         cudaStream_t s = c.stream;
-        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
+        upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
         unsigned long long* dp = grow<unsigned long long>(c.tmp[0], 2 * n_pairs);
         h2d(c, dp, pairs, 16 * n_pairs);
         uint32_t* fl = grow<uint32_t>(c.tmp[1], 4 * n_pairs);
@@ -1411,7 +1431,7 @@ int ccdk_scene_upload(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_
     return guard(ctx, [&] {
         std::lock_guard<std::mutex> lk(ctx->mu);
         CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
-        upload_scene(*ctx, v0, v1, nv, edges, ne, faces, nf);
+        upload_scene(*ctx, ctx->resident, v0, v1, nv, edges, ne, faces, nf);
         sync(*ctx);
     });
 }
@@ -1422,11 +1442,11 @@ int ccdk_ccd_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t shar
     return guard(ctx, [&] {
         std::lock_guard<std::mutex> lk(ctx->mu);
         CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
-        if (!ctx->scene.valid)
+        if (!ctx->resident.valid)
             throw Error(CCDK_CONFIG, "ccdk_ccd_resident: no scene uploaded");
         if (shard_count < 1 || shard_rank >= shard_count)
             throw Error(CCDK_CONFIG, "ccdk_ccd_resident: bad shard");
-        ccd_step(*ctx, *cfg, shard_rank, shard_count, *report, nullptr);
+        ccd_step(*ctx, ctx->resident, *cfg, shard_rank, shard_count, *report, nullptr);
     });
 }
 
@@ -1445,8 +1465,8 @@ int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
         }
         cudaEvent_t start = c.events.get(EventPool::kApi);
         CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
-        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
-        ccd_step(c, *cfg, 0, 1, *report, start);
+        upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
+        ccd_step(c, c.scene, *cfg, 0, 1, *report, start);
     });
 }
 
@@ -1466,8 +1486,8 @@ int ccdk_ccd_no_zero_toi(ccdk_ctx* ctx, const double* v0, const double* v1, uint
         ccdk_pipeline_cfg first = *cfg;
         first.narrow.no_zero_toi = 0;
         validate_pipeline_cfg(first);
-        upload_scene(c, v0, v1, nv, edges, ne, faces, nf);
-        ccd_step(c, first, 0, 1, *report, nullptr);
+        upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
+        ccd_step(c, c.scene, first, 0, 1, *report, nullptr);
         if (report->toi != 0.0)
             return;
         ccdk_pipeline_cfg retry = *cfg;
@@ -1475,7 +1495,7 @@ int ccdk_ccd_no_zero_toi(ccdk_ctx* ctx, const double* v0, const double* v1, uint
         retry.narrow.min_separation = 0.0;
         retry.min_sep_mode = CCDK_MINSEP_ABSOLUTE;
         ccdk_report second;
-        ccd_step(c, retry, 0, 1, second, nullptr);
+        ccd_step(c, c.scene, retry, 0, 1, second, nullptr);
         second.toi = 0.8 * second.toi; // one IEEE RN multiply, as in pipeline.cpp:252
         second.t_cb += report->t_cb;
         second.t_bp += report->t_bp;
@@ -1511,7 +1531,7 @@ int ccdk_broad_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, uint32_t sh
     return guard(ctx, [&] {
         std::lock_guard<std::mutex> lk(ctx->mu);
         CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
-        if (!ctx->scene.valid)
+        if (!ctx->resident.valid)
             throw Error(CCDK_CONFIG, "ccdk_broad_resident: no scene uploaded");
         if (shard_count < 1 || shard_rank >= shard_count)
             throw Error(CCDK_CONFIG, "ccdk_broad_resident: bad shard");
@@ -1541,7 +1561,7 @@ int ccdk_ccd_keys_resident(ccdk_ctx* ctx, const ccdk_pipeline_cfg* cfg, const ui
     return guard(ctx, [&] {
         std::lock_guard<std::mutex> lk(ctx->mu);
         CCDK_CUDA_CHECK(cudaSetDevice(ctx->device));
-        if (!ctx->scene.valid)
+        if (!ctx->resident.valid)
             throw Error(CCDK_CONFIG, "ccdk_ccd_keys_resident: no scene uploaded");
         ccd_keys_resident(*ctx, *cfg, dev_keys, n, key_bits, *report);
     });

@@ -74,7 +74,8 @@ struct GenArgs {
     unsigned* dirty;                 // queries whose ToI dropped (duplicates allowed)
     Region reg[2][3];                // [generation parity][split dimension]
     unsigned long long cap_pairs;    // records per region buffer
-    unsigned long long sem_cap;
+    unsigned long long sem_cap;      // queue_capacity (narrowphase.cpp:299-302); ~0 = unbounded
+    unsigned long long gen_stop;     // stop after this generation (~0 = run to the end)
     NarrowScalars* sc;
     cudaGraphConditionalHandle cond; // WHILE node of the generation graph
     unsigned long long* gen_sizes;   // compacted queue size per generation (kMaxGens entries)
@@ -520,7 +521,16 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
 }
 
 // Generation end: refresh snapshots of queries whose ToI dropped, then (last
-// block) the queue bookkeeping of narrowphase.cpp:299-304.
+// block) the queue bookkeeping of narrowphase.cpp:278-304.
+//
+// The reference tests next.size() > queue_capacity AFTER removing the
+// children of queries exhausted in this generation (narrowphase.cpp:280-302),
+// and on overflow returns the per-query results folded so far.  The split
+// records of the next generation count raw children; when that raw count
+// exceeds the capacity (or the run stops at gen_stop), every block scans the
+// next generation's records once: children of exhausted queries are counted
+// (the exact next.size()) and their t.lo folded into the query's ToI — the
+// same fold the next generation would do when it drops them (idempotent).
 __global__ void k_finish(GenArgs a)
 {
     cudaGridDependencySynchronize(); // PDL: the generation kernel has completed (no-op otherwise)
@@ -533,10 +543,33 @@ __global__ void k_finish(GenArgs a)
     const unsigned long long nd = sc->dirty_n;
     const bool all = nd > sc->dirty_cap; // list overflowed: refresh every query
     const unsigned long long m = all ? sc->nq : nd;
-    for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < m;
-         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long tid = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    const unsigned long long nthreads = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long i = tid; i < m; i += nthreads) {
         const unsigned q = all ? static_cast<unsigned>(i) : a.dirty[i];
         a.snap[q] = a.toi[q];
+    }
+    const unsigned long long gen = sc->gen;
+    const unsigned long long raw_pairs = sc->next_pairs[0] + sc->next_pairs[1] + sc->next_pairs[2];
+    const bool scan = 2 * raw_pairs > a.sem_cap || gen == a.gen_stop;
+    if (scan) {
+        const int nb = static_cast<int>(gen & 1) ^ 1;
+        unsigned cnt = 0;
+        for (int d = 0; d < 3; ++d) {
+            const Region& R = a.reg[nb][d];
+            const unsigned long long nr = sc->next_pairs[d] < a.cap_pairs ? sc->next_pairs[d] : a.cap_pairs;
+            for (unsigned long long i = tid; i < nr; i += nthreads) {
+                const unsigned q = R.qid[i];
+                if (a.exh_gen[q] != kNoGen) {
+                    const double tlo = R.t[i];
+                    atomicMin(&a.toi[q], dbits(tlo));
+                    if (a.cfg.no_zero_toi && tlo == 0.0)
+                        a.zdiag[q] = 1;
+                    cnt += 2;
+                }
+            }
+        }
+        warp_add(&sc->exh_next, cnt);
     }
     __shared__ bool last;
     __syncthreads();
@@ -553,8 +586,6 @@ __global__ void k_finish(GenArgs a)
         sc->peak = compacted;
     if (sc->gen < kMaxGens)
         a.gen_sizes[sc->gen] = compacted;
-    if (compacted > a.sem_cap)
-        sc->sem_overflow = 1;
     unsigned long long raw_next = 0;
     for (int d = 0; d < 3; ++d) {
         const unsigned long long r = sc->next_pairs[d];
@@ -564,12 +595,19 @@ __global__ void k_finish(GenArgs a)
         sc->cur_pairs[d] = r > a.cap_pairs ? a.cap_pairs : r;
         sc->next_pairs[d] = 0;
     }
+    if (scan) {
+        if (2 * raw_next - sc->exh_next > a.sem_cap) // narrowphase.cpp:299-302
+            sc->sem_overflow = 1;
+        if (gen == a.gen_stop)
+            sc->stopped = 1;
+        sc->exh_next = 0;
+    }
     sc->gen += 1;
     sc->cur_n = 2 * (sc->cur_pairs[0] + sc->cur_pairs[1] + sc->cur_pairs[2]);
     sc->dirty_n = 0;
     sc->dropped = 0;
     sc->finish_ticket = 0;
-    sc->cont = (raw_next > 0 && !sc->sem_overflow && !sc->phys_overflow) ? 1 : 0;
+    sc->cont = (raw_next > 0 && !sc->sem_overflow && !sc->phys_overflow && !sc->stopped) ? 1 : 0;
     // a BFS tree is at most 3 x 1075 bisections deep; more generations than
     // that means corrupted state, never a legitimate run
     if (sc->cont && sc->gen > 4000) {
@@ -622,12 +660,16 @@ __global__ void k_init_queries(unsigned long long n, const uint8_t* kind, const 
 }
 
 // Per-query outputs and the K9 reductions (global min ToI, total_splits).
+// On a capacity overflow the per-query results are those folded when the
+// BFS stopped (the reference returns its partial per_query, narrowphase.cpp:
+// 299-302); `defaults` writes the default ToiResult instead (the seeds
+// themselves exceed the capacity, narrowphase.cpp:215-218).
 __global__ void k_outputs(unsigned long long n, const unsigned long long* toi,
                           const unsigned long long* splits, const unsigned* exh_gen,
                           const uint8_t* zdiag, unsigned long long max_splits,
-                          NarrowScalars* sc, double* toi_out, uint8_t* flags_out)
+                          NarrowScalars* sc, double* toi_out, uint8_t* flags_out, int defaults)
 {
-    const bool overflow = sc->sem_overflow != 0;
+    const bool overflow = defaults != 0;
     unsigned long long mn = kInfBits, tot = 0;
     unsigned fl = 0;
     for (unsigned long long q = blockIdx.x * blockDim.x + threadIdx.x; q < n;
@@ -923,7 +965,7 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_gri
 // interval-buffer overflow (caller halves).
 bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const double* pts,
               const double* sep, const uint32_t* qflags, double* toi_out, uint8_t* flags_out,
-              ccdk_narrow_stats& st)
+              ccdk_narrow_stats& st, uint64_t sem_cap, uint64_t gen_stop)
 {
     cudaStream_t s = c.stream;
     // interval capacity per generation; stored as split records (2 intervals
@@ -975,7 +1017,8 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
             R.dep = grow<unsigned long long>(c.iv_dep[b][d], cap_pairs);
         }
     a.cap_pairs = cap_pairs;
-    a.sem_cap = in.queue_capacity;
+    a.sem_cap = sem_cap;
+    a.gen_stop = gen_stop;
     a.sc = static_cast<NarrowScalars*>(c.nscal.ensure(sizeof(NarrowScalars)));
     a.gen_sizes = grow<unsigned long long>(c.gen_sizes, kMaxGens);
 
@@ -1035,7 +1078,7 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     // physical overflow, when the caller halves), then one read-back
     k_outputs<<<std::min<unsigned>(ig.x, 4096u), 256, 0, s>>>(n, a.toi, a.splits, a.exh_gen,
                                                               a.zdiag, a.max_splits, a.sc,
-                                                              toi_out, flags_out);
+                                                              toi_out, flags_out, 0);
     CCDK_LAUNCH_CHECK();
     NarrowScalars* host_sc = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
     CCDK_CUDA_CHECK(cudaMemcpyAsync(host_sc, a.sc, sizeof(NarrowScalars), cudaMemcpyDeviceToHost, s));
@@ -1057,7 +1100,8 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         throw Error(CCDK_CUDA, "narrow phase: generation limit exceeded (internal error)");
     if (host_sc->phys_overflow)
         return false;
-    st.overflow = host_sc->sem_overflow ? 1 : 0;
+    if (host_sc->sem_overflow) // sticky across the runs of one narrow phase
+        st.overflow = 1;
     const double g = __builtin_bit_cast(double, static_cast<uint64_t>(host_sc->global_toi_bits));
     st.global_toi = st.overflow ? INFINITY : std::min(st.global_toi, g);
     st.peak_queue = std::max<uint64_t>(st.peak_queue, std::max<uint64_t>(host_sc->peak, n));
@@ -1077,20 +1121,27 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     return true;
 }
 
+constexpr uint64_t kNoStop = ~0ull;
+
+// Run queries [lo, hi) to completion, halving on a physical interval-buffer
+// overflow; `leaves` receives the query ranges that completed.
 void run_range(Ctx& c, const NarrowIn& in, uint64_t lo, uint64_t hi, double* toi_out,
-               uint8_t* flags_out, ccdk_narrow_stats& st)
+               uint8_t* flags_out, ccdk_narrow_stats& st, uint64_t sem_cap, uint64_t gen_stop,
+               std::vector<std::pair<uint64_t, uint64_t>>& leaves)
 {
     const uint64_t n = hi - lo;
     if (n == 0)
         return;
     if (run_once(c, in, n, in.kind + lo, in.points + 24 * lo, in.sep ? in.sep + lo : nullptr,
-                 in.qflags ? in.qflags + lo : nullptr, toi_out + lo, flags_out + lo, st))
+                 in.qflags ? in.qflags + lo : nullptr, toi_out + lo, flags_out + lo, st, sem_cap, gen_stop)) {
+        leaves.emplace_back(lo, hi);
         return;
+    }
     if (n <= 1)
         throw Error(CCDK_CAPACITY, "narrow phase: interval buffer cannot hold one query's frontier");
     const uint64_t mid = lo + n / 2;
-    run_range(c, in, lo, mid, toi_out, flags_out, st);
-    run_range(c, in, mid, hi, toi_out, flags_out, st);
+    run_range(c, in, lo, mid, toi_out, flags_out, st, sem_cap, gen_stop, leaves);
+    run_range(c, in, mid, hi, toi_out, flags_out, st, sem_cap, gen_stop, leaves);
 }
 
 } // namespace
@@ -1108,6 +1159,7 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
         c.gen_acc.clear();
     cudaEvent_t e0 = c.events.get(EventPool::kNarrow), e1 = c.events.get(EventPool::kNarrow + 1);
     CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+    const bool bounded = in.queue_capacity != UINT64_MAX;
     if (n > 0 && n > in.queue_capacity) {
         // narrowphase.cpp:215-218: seeds alone exceed the capacity
         st.overflow = 1;
@@ -1122,23 +1174,61 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
         unsigned long long* dummy = grow<unsigned long long>(c.toi_live, n);
         k_outputs<<<std::min<unsigned>(g.x, 4096u), 256, 0, c.stream>>>(
             n, dummy, dummy, grow<unsigned>(c.exh_gen, n), grow<uint8_t>(c.zdiag, n), 0, sc,
-            out.toi, out.flags);
+            out.toi, out.flags, 1);
         CCDK_LAUNCH_CHECK();
     } else if (n > 0) {
-        run_range(c, in, 0, n, out.toi, out.flags, st);
+        std::vector<std::pair<uint64_t, uint64_t>> leaves;
+        const std::vector<uint64_t> acc0 = c.gen_acc; // chunked callers' sums so far
+        run_range(c, in, 0, n, out.toi, out.flags, st, in.queue_capacity, kNoStop, leaves);
+        if (bounded && leaves.size() > 1) {
+            // The batch ran as several device runs (physical halving), each
+            // checked against the capacity on its own; the reference checks
+            // the WHOLE batch's queue per generation (narrowphase.cpp:299-302).
+            // A part's queue never exceeds the whole's, so a part overflowing
+            // means the whole overflowed at the same or an earlier
+            // generation.  Re-decide on the summed per-generation sizes:
+            // complete them first if a part stopped early (re-run unbounded),
+            // then, if some generation g's summed queue exceeds the capacity,
+            // the reference stopped after generation g-1: re-run every part to
+            // exactly that generation for its partial per-query results.
+            auto summed = [&](size_t g) { return c.gen_acc[g] - (g < acc0.size() ? acc0[g] : 0); };
+            auto rerun = [&](uint64_t gen_stop) {
+                c.gen_acc = acc0;
+                ccdk_narrow_stats s2 {};
+                s2.global_toi = INFINITY;
+                std::vector<std::pair<uint64_t, uint64_t>> refined;
+                for (auto& lf : leaves)
+                    run_range(c, in, lf.first, lf.second, out.toi, out.flags, s2, UINT64_MAX, gen_stop, refined);
+                leaves.swap(refined);
+                st = s2;
+            };
+            if (st.overflow)
+                rerun(kNoStop);
+            uint64_t first = kNoStop;
+            for (size_t g = 1; g < c.gen_acc.size(); ++g)
+                if (summed(g) > in.queue_capacity) {
+                    first = g;
+                    break;
+                }
+            if (first != kNoStop) {
+                rerun(first - 1);
+                st.overflow = 1;
+            }
+        }
     }
     CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
     CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
     float ms = 0;
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
     st.device_ms = ms;
-    if (st.overflow) {
-        st.global_toi = INFINITY;
-    } else if (n > 0) {
+    if (n > 0 && !(n > in.queue_capacity)) {
+        // narrowphase.cpp:227, 303: max over the (summed) generation queues
         st.peak_queue = 0;
         for (uint64_t v : c.gen_acc)
             st.peak_queue = std::max<uint64_t>(st.peak_queue, v);
     }
+    if (st.overflow)
+        st.global_toi = INFINITY; // left at kNoCollision on overflow (narrowphase.cpp:307-309)
     out.stats = st;
     out.launches = c.narrow_launches;
     out.any_flags = st.overflow ? 0 : c.narrow_any_flags;

@@ -81,12 +81,17 @@ __device__ void mean_from_partials(const double* part, unsigned long long k, dou
 __global__ void __launch_bounds__(kRedThreads) k_axis_sum(const float* bmin, const float* bmax,
                                                           unsigned long long k, double* part)
 {
-    double v[3] = { 0, 0, 0 };
+    double v[3] = { 0, 0, 0 }, a[3] = { 0, 0, 0 };
     for (unsigned long long s = blockIdx.x * kRedThreads + threadIdx.x; s < k;
          s += kRedBlocks * kRedThreads)
-        for (int c = 0; c < 3; ++c)
-            v[c] = __dadd_rn(v[c], centre(bmin, bmax, k, c, s));
+        for (int c = 0; c < 3; ++c) {
+            const double x = centre(bmin, bmax, k, c, s);
+            v[c] = __dadd_rn(v[c], x);
+            a[c] = __dadd_rn(a[c], fabs(x));
+        }
     block_sum3(v, part + 3 * blockIdx.x);
+    __syncthreads();
+    block_sum3(a, part + 6 * kRedBlocks + 3 * blockIdx.x); // sum |c| for the error bound
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_axis_var(const float* bmin, const float* bmax,
@@ -106,21 +111,110 @@ __global__ void __launch_bounds__(kRedThreads) k_axis_var(const float* bmin, con
     block_sum3(v, vpart + 3 * blockIdx.x);
 }
 
-__global__ void __launch_bounds__(kRedThreads) k_axis_pick(const double* vpart, int* axis)
+// gamma_m = m u / (1 - m u), u = 2^-53 (Higham's bound for m roundings)
+__device__ __forceinline__ double gamma_n(double m)
 {
-    double v[3] = { 0, 0, 0 };
+    const double mu = m * 0x1p-53;
+    return mu / (1.0 - mu);
+}
+
+// Argmax of the tree-summed variances, and whether the reference's SERIAL
+// sums (broadphase.cpp:45-67) could order the axes differently.  For either
+// summation order, with n = k, A = sum |c_i| and exact mean mu:
+//   |mean_hat - mu| <= dm = gamma_{n+1} A / n
+//   V_hat = sum (c_i - mean_hat)^2 (1 + theta_{n+2}),
+//   sum (c_i - mean_hat)^2 = V* + n (mean_hat - mu)^2     (V* exact),
+// so serial and tree variances differ by at most 2 gamma_{n+2} V + 2 n dm^2
+// (+ second order); R below is twice that.  If the chosen axis's interval
+// [V - R, V + R] is disjoint from every other axis's, the serial argmax
+// (strict '>', ties to the lower axis) is the same axis; otherwise flag
+// the serial recomputation (k_axis_serial).
+__global__ void __launch_bounds__(kRedThreads) k_axis_pick(const double* part, unsigned long long k,
+                                                           int* axis)
+{
+    const double* vpart = part + 3 * kRedBlocks;
+    const double* apart = part + 6 * kRedBlocks;
+    double v[3] = { 0, 0, 0 }, a[3] = { 0, 0, 0 };
     for (int b = threadIdx.x; b < kRedBlocks; b += kRedThreads)
-        for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < 3; ++c) {
             v[c] = __dadd_rn(v[c], vpart[3 * b + c]);
-    __shared__ double var[3];
+            a[c] = __dadd_rn(a[c], apart[3 * b + c]);
+        }
+    __shared__ double var[3], abs_sum[3];
     block_sum3(v, var);
     __syncthreads();
+    block_sum3(a, abs_sum);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        int a = 0;
+        int best = 0;
         for (int c = 1; c < 3; ++c)
-            if (var[c] > var[a])
-                a = c;
-        *axis = a;
+            if (var[c] > var[best])
+                best = c;
+        const double n = static_cast<double>(k);
+        const double g = gamma_n(n + 3.0);
+        double R[3];
+        for (int c = 0; c < 3; ++c) {
+            const double dm = gamma_n(n + 2.0) * abs_sum[c] * (1.0 + 4.0 * g) / n;
+            R[c] = 4.0 * g * var[c] + 4.0 * n * dm * dm + 0x1p-1000;
+        }
+        int uncertain = 0;
+        for (int c = 0; c < 3; ++c)
+            if (c != best && var[best] - R[best] <= var[c] + R[c])
+                uncertain = 1;
+        axis[0] = best;
+        axis[1] = uncertain;
+    }
+}
+
+// The reference's choose_axis in its own summation order, for inputs whose
+// tree-summed variances are within the error bound of a tie (regular meshes
+// without jitter: symmetric extents give equal variances up to rounding).
+// One warp per axis; the warp stages 1024 centres in shared memory and lane 0
+// adds them in index order, so the result is bit-identical to the serial
+// loop.  Runs (and costs ~2 dependent DADDs per box) only when axis[1] is set.
+constexpr int kSerialChunk = 1024;
+__global__ void __launch_bounds__(96) k_axis_serial(const float* bmin, const float* bmax,
+                                                   unsigned long long k, int* axis)
+{
+    if (!axis[1])
+        return;
+    __shared__ double stage[3][kSerialChunk];
+    __shared__ double var[3];
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* st = stage[c];
+    double mean = 0.0, acc = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        acc = 0.0;
+        for (unsigned long long s0 = 0; s0 < k; s0 += kSerialChunk) {
+            const unsigned long long cnt = k - s0 < kSerialChunk ? k - s0 : kSerialChunk;
+            for (unsigned long long i = lane; i < cnt; i += 32)
+                st[i] = centre(bmin, bmax, k, c, s0 + i);
+            __syncwarp();
+            if (lane == 0) {
+                if (pass == 0) {
+                    for (unsigned long long i = 0; i < cnt; ++i)
+                        acc = __dadd_rn(acc, st[i]);
+                } else {
+                    for (unsigned long long i = 0; i < cnt; ++i) {
+                        const double d = __dsub_rn(st[i], mean);
+                        acc = __dadd_rn(acc, __dmul_rn(d, d));
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        mean = __shfl_sync(0xffffffffu, __ddiv_rn(acc, static_cast<double>(k)), 0);
+    }
+    if (lane == 0)
+        var[c] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int a = 1; a < 3; ++a)
+            if (var[a] > var[best])
+                best = a;
+        axis[0] = best;
+        axis[2] = 1; // the serial order decided
     }
 }
 
@@ -644,11 +738,19 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     CCDK_CUDA_CHECK(cudaMemsetAsync(ctr->misc, 0, sizeof ctr->misc, s));
 
     // K2 choose_axis
+    // d_axis[0] = axis, [1] = near tie (serial recomputation needed), [2] = serial ran
     int* d_axis = static_cast<int*>(c.axis.ensure(64));
-    double* part = grow<double>(c.partials, 6 * kRedBlocks);
+    double* part = grow<double>(c.partials, 9 * kRedBlocks);
+    CCDK_CUDA_CHECK(cudaMemsetAsync(d_axis, 0, 4 * sizeof(int), s));
     k_axis_sum<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, part);
     k_axis_var<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, part, part + 3 * kRedBlocks);
-    k_axis_pick<<<1, kRedThreads, 0, s>>>(part + 3 * kRedBlocks, d_axis);
+    k_axis_pick<<<1, kRedThreads, 0, s>>>(part, k, d_axis);
+    // The candidate set does not depend on the axis; the axis is observable
+    // only through choose_axis itself, StqStats and SweepRange slices (and the
+    // budget batching built on them), so the exact serial order is enforced
+    // where those are requested.
+    if (in.exact_axis)
+        k_axis_serial<<<1, 96, 0, s>>>(in.bmin, in.bmax, k, d_axis);
     CCDK_LAUNCH_CHECK();
 
     // K3 sort + permute
@@ -825,13 +927,15 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         }
     }
     CCDK_CUDA_CHECK(cudaEventRecord(ev[3], s));
-    int axis = 0;
-    CCDK_CUDA_CHECK(cudaMemcpyAsync(&axis, d_axis, sizeof axis, cudaMemcpyDeviceToHost, s));
+    int axis[4] = { 0, 0, 0, 0 };
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(axis, d_axis, sizeof axis, cudaMemcpyDeviceToHost, s));
     CCDK_CUDA_CHECK(cudaEventSynchronize(ev[3]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_axis_sort, ev[0], ev[1]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_sweep, ev[1], ev[2]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_pairsort, ev[2], ev[3]));
-    out.axis = axis;
+    out.axis = axis[0];
+    out.axis_near_tie = axis[1] != 0;
+    out.axis_serial = axis[2] != 0;
     out.n_pairs = n_pairs;
     c.last_n_pairs = n_pairs;
 }

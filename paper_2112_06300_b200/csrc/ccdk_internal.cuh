@@ -203,6 +203,8 @@ struct NarrowScalars {
     unsigned long long dirty_cap;     // dirty-list capacity; beyond it every query is refreshed
     unsigned long long cur_pairs[3];  // split records per region in the current generation
     unsigned long long next_pairs[3]; // append cursors of the next generation
+    unsigned long long exh_next;      // next-generation intervals of exhausted queries (exact-size scans)
+    unsigned long long stopped;       // the run stopped at GenArgs::gen_stop
 };
 
 // The narrow phase's generation loop as one CUDA graph: a WHILE conditional
@@ -248,6 +250,8 @@ struct BroadOut {
     uint64_t pair_tests = 0;
     uint64_t range_lo = 0, range_hi = 0; // sorted left positions actually swept
     int axis = 0;
+    bool axis_near_tie = false; // tree-summed variances within the error bound of a tie
+    bool axis_serial = false;   // ... and the reference's serial order decided the axis
     float ms_axis_sort = 0, ms_sweep = 0, ms_pairsort = 0;
 };
 // General broad phase over SoA boxes whose slot order is owner order (rank =
@@ -263,6 +267,9 @@ struct BroadIn {
     uint32_t shard_rank = 0, shard_count = 1;
     bool want_rounds = false;
     bool unique = false; // duplicate owners possible
+    // reproduce choose_axis's serial summation order on near ties (the axis
+    // is observable through choose_axis, StqStats and SweepRange slices)
+    bool exact_axis = true;
 };
 void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out);
 
@@ -317,7 +324,9 @@ struct Ctx {
     std::mutex mu;
     uint64_t interval_capacity = 0; // 0 = auto
 
-    DevScene scene;
+    DevScene scene;                    // per-call uploads (ccdk_ccd, ccdk_build_boxes, ccdk_classify, ...)
+    DevScene resident;                 // ccdk_scene_upload's scene: only the *_resident calls use it
+    uint64_t last_nv = 0, last_ne = 0; // id offsets of the scene behind the last pair list
 
     // boxes / broad phase
     DevBuf bmin, bmax, vids, raw;      // slot order

@@ -476,7 +476,11 @@ CCDKIT_EXPORT void PipelineConfig::validate() const
 CCDKIT_EXPORT CcdReport ccd(const SceneStep& scene, const PipelineConfig& cfg)
 {
     cfg.validate();
-    scene.validate();
+    // SceneStep::validate's element checks run on the device right after the
+    // upload (k_validate_scene, same first-failure order and messages); only
+    // the snapshot-length check needs the host containers
+    if (scene.vertices_t0.size() != scene.vertices_t1.size())
+        throw InvalidInput("vertex snapshots differ in length");
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
     SequenceGuard g(sequence_mutex());
@@ -516,7 +520,8 @@ CCDKIT_EXPORT CcdReport ccd_no_zero_toi(const SceneStep& scene, const PipelineCo
 {
     if (!cfg.narrow.no_zero_toi)
         throw ConfigError("ccd_no_zero_toi: cfg.narrow.no_zero_toi must be set");
-    scene.validate();
+    if (scene.vertices_t0.size() != scene.vertices_t1.size()) // element checks: on the device
+        throw InvalidInput("vertex snapshots differ in length");
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
     SequenceGuard g(sequence_mutex());

@@ -74,6 +74,21 @@ def allreduce_min_toi(toi_tensor, group=None):
     return toi_tensor
 
 
+def bind_to_torch_stream(resident):
+    """Stream contract of the multi-GPU layer: the context runs on torch's
+    current stream of its device, so the context's kernels and copies
+    (ccdk_copy_last_toi, ccdk_copy_keys_device, the narrow phase's sort of
+    the received keys) are stream-ordered with the collectives torch issues
+    (NCCL waits on the current stream; its outputs are ready for the next
+    work enqueued there).  Without it, a context on its own non-blocking
+    stream could allreduce a ToI before the copy lands, or sort keys
+    all_to_all has not delivered yet."""
+    import torch
+    dev = torch.device(f"cuda:{resident.ctx.device}")
+    resident.ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    return dev
+
+
 class ShardedCcd:
     """Runs the device-resident CCD step for this rank's shard and combines
     the global ToI across ranks on the device."""
@@ -83,7 +98,8 @@ class ShardedCcd:
         self.resident = resident
         self.rank = rank
         self.world = world
-        self.toi = torch.full((1,), float("inf"), dtype=torch.float64, device=f"cuda:{resident.ctx.device}")
+        dev = bind_to_torch_stream(resident)
+        self.toi = torch.full((1,), float("inf"), dtype=torch.float64, device=dev)
 
     def step(self, cfg):
         rep = self.resident.step(cfg, self.rank, self.world)
@@ -143,7 +159,7 @@ class RebalancedCcd:
         self.rank = rank
         self.world = world
         self.group = group
-        self.dev = f"cuda:{resident.ctx.device}"
+        self.dev = bind_to_torch_stream(resident)
         self.toi = torch.full((1,), float("inf"), dtype=torch.float64, device=self.dev)
         self.keys = torch.empty(0, dtype=torch.int64, device=self.dev)
 
@@ -152,9 +168,9 @@ class RebalancedCcd:
         import torch.distributed as dist
         n, nb, broad_ms = self.resident.broad(cfg, self.rank, self.world)
         cnt = torch.tensor([n], dtype=torch.int64, device=self.dev)
-        counts = [torch.zeros(1, dtype=torch.int64, device=self.dev) for _ in range(self.world)]
-        dist.all_gather(counts, cnt, group=self.group)
-        counts = [int(c.item()) for c in counts]
+        gathered = torch.empty(self.world, dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(gathered, cnt, group=self.group)
+        counts = [int(c) for c in gathered.cpu().tolist()]  # one read-back for all N counts
         if self.keys.numel() < max(n, 1):
             self.keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
         self.resident.copy_keys(self.keys.data_ptr())
