@@ -240,6 +240,26 @@ CCDK_API int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_
              const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
              const ccdk_pipeline_cfg* cfg, ccdk_report* report);
 
+/* Candidate export for ccdk_ccd_into.  Called exactly once per step with the
+ * final canonical candidate list in pinned host memory that is valid only
+ * during the call: 16 bytes per pair, left id then right id, each id
+ * {uint8 kind, 3 zero bytes, uint32 index} (= kind | index << 32 as a
+ * little-endian u64, the in-memory layout of ccdkit::CandidatePair on
+ * x86-64).  When the step needs a single broad batch (always at the default
+ * memory budget) the sink runs on a library worker thread WHILE the device
+ * runs classify + narrow phase, so a caller's allocation and copy of the
+ * list overlap the GPU; otherwise it runs on the calling thread before
+ * ccdk_ccd_into returns.  Return 0, or nonzero to fail the call with
+ * CCDK_OOM (e.g. the caller could not allocate). */
+typedef int (*ccdk_pairs_sink)(void* user, const uint64_t* pairs, uint64_t n_pairs);
+
+/* ccd returning the candidate list through `sink` (the drop-in's
+ * ccdkit::ccd: CcdReport::candidates, pipeline.cpp:209). */
+CCDK_API int ccdk_ccd_into(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+                           const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
+                           const ccdk_pipeline_cfg* cfg, ccdk_report* report, ccdk_pairs_sink sink,
+                           void* user);
+
 /* ccd_no_zero_toi (pipeline.hpp:82-85, pipeline.cpp:234-256): requires
  * cfg->narrow.no_zero_toi; a separated run, then on an exact-zero ToI a
  * zero-separation always-split-at-t=0 retry whose ToI is scaled by 0.8. */

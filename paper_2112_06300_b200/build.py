@@ -3,8 +3,10 @@
     libccdk.so    CUDA kernels + the C ABI (include/ccdk.h)
     libccdkit.so  C++ host API with the reference signatures
                   (include/ccdkit/*.hpp) layered on libccdk.so
+                  incl. the benchmark/audit layer (bench.hpp, OBJ ingestion)
     libccdkit_bench.so  end-to-end timing harness: ccdkit::ccd through
                   libccdkit.so from pageable host vectors (bench.py e2e)
+    ccdbench      the audit/benchmark CLI over libccdkit.so (no oracle linked)
 
 Both land in paper_2112_06300_b200/lib/ so they travel with the repository
 snapshot to the GPU box.  Flags: no FMA contraction (--fmad=false, and the
@@ -24,7 +26,7 @@ INCLUDE = os.path.join(ROOT, "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CU_SOURCES = ["ccdk_api.cu", "ccdk_geometry.cu", "ccdk_broad.cu", "ccdk_bfs.cu", "ccdk_distance.cu"]
-CXX_SOURCES = ["ccdkit_host.cpp"]
+CXX_SOURCES = ["ccdkit_host.cpp", "ccdkit_audit.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
@@ -69,13 +71,19 @@ def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False) 
         _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", so,
               "-cudart", "static"], verbose)
     # C++ host API over the C ABI
-    cxx = os.path.join(CSRC, "ccdkit_host.cpp")
+    cxx = [os.path.join(CSRC, c) for c in CXX_SOURCES]
     so2 = os.path.join(LIB, "libccdkit.so")
     ccdkit_headers = [os.path.join(INCLUDE, "ccdkit", h) for h in os.listdir(os.path.join(INCLUDE, "ccdkit"))] \
         if os.path.isdir(os.path.join(INCLUDE, "ccdkit")) else []
-    if os.path.exists(cxx) and (force or _stale(so2, [cxx, so] + ccdkit_headers)):
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, cxx, "-o", so2,
+    if force or _stale(so2, cxx + [so] + ccdkit_headers):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, *cxx, "-o", so2,
               "-L", LIB, "-lccdk", "-Wl,-rpath,$ORIGIN"], verbose)
+    # the audit / benchmark CLI (proj/tools/ccdbench.cpp's interface)
+    cb = os.path.join(CSRC, "ccdbench.cpp")
+    exe = os.path.join(LIB, "ccdbench")
+    if force or _stale(exe, [cb, so2] + ccdkit_headers):
+        _run(["g++", "-std=c++20", "-O2", "-I", INCLUDE, cb, "-o", exe,
+              "-L", LIB, "-lccdkit", "-lccdk", "-Wl,-rpath,$ORIGIN"], verbose)
     # end-to-end timing harness over the drop-in (bench.py's e2e leg)
     hb = os.path.join(CSRC, "ccdkit_bench.cpp")
     so3 = os.path.join(LIB, "libccdkit_bench.so")

@@ -376,6 +376,54 @@ void upload_scene(Ctx& c, DevScene& s, const double* v0, const double* v1, uint6
     s.valid = true;
 }
 
+// ---- candidate export (ccdk_ccd_into).  The final canonical key list is
+// converted to ccdkit::CandidatePair's layout on the device, copied into
+// pinned staging on the copy stream, and handed to the caller's sink — on a
+// worker thread while the compute stream runs classify + narrow phase (single
+// broad batch), or inline at the end of the step (batched steps).
+void export_begin(Ctx& c, const uint64_t* keys, uint64_t n, uint64_t nv, uint64_t ne, bool async)
+{
+    PairExport& x = *c.exp;
+    x.started = true;
+    if (!c.copy_stream)
+        CCDK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    void* pin = c.pin_pairs.ensure(std::max<uint64_t>(16 * n, 16));
+    cudaEvent_t ready = c.events.get(EventPool::kExport), done = c.events.get(EventPool::kExport + 1);
+    if (n) {
+        uint64_t* ids = grow<uint64_t>(c.pair_ids, 2 * n);
+        launch_keys_to_ids(c, keys, n, c.last_nb, nullptr, nullptr, nv, ne, ids, 1);
+        CCDK_CUDA_CHECK(cudaEventRecord(ready, c.stream));
+        CCDK_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, ready, 0));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(pin, ids, 16 * n, cudaMemcpyDeviceToHost, c.copy_stream));
+    }
+    CCDK_CUDA_CHECK(cudaEventRecord(done, c.copy_stream));
+    const int device = c.device;
+    auto deliver = [&x, pin, n, done, device] {
+        cudaSetDevice(device);
+        const cudaError_t r = cudaEventSynchronize(done);
+        if (r != cudaSuccess) {
+            x.error = std::string("candidate export: ") + cudaGetErrorString(r);
+            return;
+        }
+        x.sink_rc = x.sink(x.user, static_cast<const uint64_t*>(pin), n);
+    };
+    if (async)
+        x.worker = std::thread(deliver);
+    else
+        deliver();
+}
+
+void export_finish(Ctx& c)
+{
+    PairExport& x = *c.exp;
+    if (x.worker.joinable())
+        x.worker.join();
+    if (!x.error.empty())
+        throw Error(CCDK_CUDA, x.error);
+    if (x.sink_rc)
+        throw Error(CCDK_OOM, "ccdk_ccd_into: the candidate sink failed");
+}
+
 // run_batched's BatchRun (pipeline.cpp:81-175) over device primitives.  The
 // recursion structure, capacities and counters follow the reference so the
 // batch count and tracked bytes agree; every broad/narrow batch is a device
@@ -432,6 +480,9 @@ struct BatchRun {
             broad_batch(mid, end);
             return;
         }
+        // the whole step in one broad batch: these keys are the final list
+        if (c.exp && !c.exp->started && broad_batches == 0 && begin == 0 && end >= k && shard_count == 1)
+            export_begin(c, c.pair_keys_sorted.as<uint64_t>(), bo.n_pairs, s.nv, s.ne, true);
         ++broad_batches;
         process_keys(c.pair_keys_sorted.as<uint64_t>(), bo.n_pairs);
     }
@@ -593,6 +644,11 @@ void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_
         });
         CCDK_CUDA_CHECK(cudaMemcpyAsync(all, tmp, run.candidates * 8, cudaMemcpyDeviceToDevice, st));
     }
+    if (c.exp) {
+        if (!c.exp->started)
+            export_begin(c, c.all_keys.as<uint64_t>(), run.candidates, s.nv, s.ne, false);
+        export_finish(c);
+    }
     c.last_keys_all = true;
     c.last_pairs_general = false;
     c.last_n_pairs = run.candidates;
@@ -726,6 +782,11 @@ void ccd_keys_resident(Ctx& c, const ccdk_pipeline_cfg& cfg, const uint64_t* key
     const uint64_t cap_pairs = ~0ull;
     BatchRun run { c, cfg, s, k, cap_pairs };
     run.process_keys(sorted, n);
+    if (c.exp) {
+        if (!c.exp->started)
+            export_begin(c, c.all_keys.as<uint64_t>(), run.candidates, s.nv, s.ne, false);
+        export_finish(c);
+    }
     c.last_keys_all = true;
     c.last_pairs_general = false;
     c.last_n_pairs = run.candidates;
@@ -1463,6 +1524,41 @@ int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
             if (nv)
                 throw Error(CCDK_INVALID_INPUT, "vertex snapshots missing");
         }
+        cudaEvent_t start = c.events.get(EventPool::kApi);
+        CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
+        upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
+        ccd_step(c, c.scene, *cfg, 0, 1, *report, start);
+    });
+}
+
+int ccdk_ccd_into(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv, const uint32_t* edges,
+                  uint64_t ne, const uint32_t* faces, uint64_t nf, const ccdk_pipeline_cfg* cfg,
+                  ccdk_report* report, ccdk_pairs_sink sink, void* user)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        validate_pipeline_cfg(*cfg);
+        if (!sink)
+            throw Error(CCDK_INVALID_INPUT, "ccdk_ccd_into: sink is null");
+        if (!v0 || !v1) {
+            if (nv)
+                throw Error(CCDK_INVALID_INPUT, "vertex snapshots missing");
+        }
+        PairExport x;
+        x.sink = sink;
+        x.user = user;
+        struct Scope { // never leave with the worker running
+            Ctx& c;
+            ~Scope()
+            {
+                if (c.exp && c.exp->worker.joinable())
+                    c.exp->worker.join();
+                c.exp = nullptr;
+            }
+        } scope { c };
+        c.exp = &x;
         cudaEvent_t start = c.events.get(EventPool::kApi);
         CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
         upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);

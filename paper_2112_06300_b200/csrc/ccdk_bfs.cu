@@ -849,7 +849,7 @@ __global__ void k_records_to_internal(const double* __restrict__ ref, unsigned l
 __global__ void k_keys_to_ids(const unsigned long long* keys, unsigned long long n, int nb,
                               const uint8_t* own_kind, const uint32_t* own_index,
                               unsigned long long nv, unsigned long long ne,
-                              unsigned long long* ids)
+                              unsigned long long* ids, int layout)
 {
     const unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (i >= n)
@@ -864,6 +864,8 @@ __global__ void k_keys_to_ids(const unsigned long long* keys, unsigned long long
             const unsigned long long x = r[s];
             id = x < nv ? x : x < nv + ne ? ((1ull << 32) | (x - nv)) : ((2ull << 32) | (x - nv - ne));
         }
+        if (layout == 1) // {u8 kind, 3 zero bytes, u32 index}
+            id = (id >> 32) | (id << 32);
         ids[2 * i + s] = id;
     }
 }
@@ -1308,13 +1310,14 @@ void launch_records_to_internal(Ctx& c, const double* ref, uint64_t n, double* i
 }
 
 void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb, const uint8_t* own_kind,
-                        const uint32_t* own_index, uint64_t nv, uint64_t ne, uint64_t* ids)
+                        const uint32_t* own_index, uint64_t nv, uint64_t ne, uint64_t* ids, int layout,
+                        cudaStream_t stream)
 {
     if (!n)
         return;
-    k_keys_to_ids<<<grid_for(n, 256), 256, 0, c.stream>>>(
+    k_keys_to_ids<<<grid_for(n, 256), 256, 0, stream ? stream : c.stream>>>(
         reinterpret_cast<const unsigned long long*>(keys), n, nb, own_kind, own_index, nv, ne,
-        reinterpret_cast<unsigned long long*>(ids));
+        reinterpret_cast<unsigned long long*>(ids), layout);
     CCDK_LAUNCH_CHECK();
 }
 

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ccdk.h"
@@ -142,7 +143,7 @@ struct PinnedBuf {
 // call takes driver locks; fixed slots per call site, each slot's use is
 // synchronised before its next record).
 struct EventPool {
-    enum { kStep = 0, kBatch = 6, kBroad = 8, kNarrow = 12, kApi = 16, kSlots = 20 };
+    enum { kStep = 0, kBatch = 6, kBroad = 8, kNarrow = 12, kApi = 16, kExport = 20, kSlots = 22 };
     cudaEvent_t ev[kSlots] = {};
     EventPool() = default;
     EventPool(const EventPool&) = delete;
@@ -310,9 +311,22 @@ void launch_min_seps(Ctx& c, const uint8_t* kind, const double* pts, uint64_t n,
 void launch_copy_device(Ctx& c, const void* src, void* dst, uint64_t bytes);
 // reference-order query records -> narrow-phase internal order
 void launch_records_to_internal(Ctx& c, const double* ref, uint64_t n, double* il);
+// layout 0: (kind << 32) | index per id (C ABI); layout 1: kind | index << 32
+// (ccdkit::CandidatePair's in-memory layout, the ccdk_pairs_sink contract)
 void launch_keys_to_ids(Ctx& c, const uint64_t* keys, uint64_t n, int nb,
                         const uint8_t* own_kind, const uint32_t* own_index, uint64_t nv,
-                        uint64_t ne, uint64_t* ids);
+                        uint64_t ne, uint64_t* ids, int layout = 0, cudaStream_t stream = nullptr);
+
+// Candidate export of ccdk_ccd_into: the final pair list goes to the caller's
+// sink from pinned staging, overlapping the narrow phase when possible.
+struct PairExport {
+    ccdk_pairs_sink sink = nullptr;
+    void* user = nullptr;
+    bool started = false;
+    int sink_rc = 0;
+    std::string error;
+    std::thread worker;
+};
 
 // ------------------------------------------------------------------ context
 
@@ -372,6 +386,11 @@ struct Ctx {
     // pipeline results across batches
     DevBuf all_keys, all_toi, all_flags;
     bool last_keys_all = false; // fetch_pairs reads all_keys (pipeline) or pair_keys_sorted (API)
+
+    // candidate export (ccdk_ccd_into)
+    PairExport* exp = nullptr;
+    DevBuf pair_ids;
+    PinnedBuf pin_pairs;
 
     // staging for API calls
     DevBuf tmp[8];

@@ -17,8 +17,10 @@
 #include "ccdkit/pipeline.hpp"
 #include "ccdkit/scene.hpp"
 
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <stdexcept>
 
@@ -473,6 +475,36 @@ CCDKIT_EXPORT void PipelineConfig::validate() const
         throw ConfigError("PipelineConfig: inflation must be >= 0");
 }
 
+// ccdk_ccd_into's sink: the pinned pair list is in CandidatePair's own layout
+// ({u8 kind, pad, u32 index} x 2), so the report's vector is filled by one
+// copy — on the library's worker thread, while the device runs the narrow
+// phase.
+static_assert(sizeof(PrimitiveId) == 8 && offsetof(PrimitiveId, index) == 4 && sizeof(CandidatePair) == 16
+                  && offsetof(CandidatePair, right) == 8,
+              "CandidatePair layout differs from the ccdk_pairs_sink contract");
+
+namespace {
+
+struct CandidateSink {
+    std::vector<CandidatePair>* out;
+    std::exception_ptr err;
+};
+
+int candidate_sink(void* user, const uint64_t* pairs, uint64_t n)
+{
+    auto* st = static_cast<CandidateSink*>(user);
+    try {
+        const auto* p = reinterpret_cast<const CandidatePair*>(pairs);
+        st->out->assign(p, p + n);
+        return 0;
+    } catch (...) {
+        st->err = std::current_exception();
+        return 1;
+    }
+}
+
+} // namespace
+
 CCDKIT_EXPORT CcdReport ccd(const SceneStep& scene, const PipelineConfig& cfg)
 {
     cfg.validate();
@@ -483,10 +515,18 @@ CCDKIT_EXPORT CcdReport ccd(const SceneStep& scene, const PipelineConfig& cfg)
         throw InvalidInput("vertex snapshots differ in length");
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
+    std::vector<CandidatePair> cands;
+    CandidateSink sink { &cands, nullptr };
     SequenceGuard g(sequence_mutex());
-    check(ccdk_ccd(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1), scene.vertices_t0.size(),
-                   edata(scene), scene.edges.size(), fdata(scene), scene.faces.size(), &c, &r));
-    return to_report(r, true);
+    const int rc = ccdk_ccd_into(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1),
+                                 scene.vertices_t0.size(), edata(scene), scene.edges.size(), fdata(scene),
+                                 scene.faces.size(), &c, &r, candidate_sink, &sink);
+    if (sink.err)
+        std::rethrow_exception(sink.err);
+    check(rc);
+    CcdReport rep = to_report(r, false);
+    rep.candidates = std::move(cands);
+    return rep;
 }
 
 CCDKIT_EXPORT ToiResult run_batched(const SceneStep& scene, const std::vector<Aabb>& boxes,
