@@ -182,10 +182,12 @@ CcdReport to_report(const ccdk_report& r, bool with_candidates)
     rep.tracked_peak_bytes = r.tracked_peak_bytes;
     if (with_candidates)
         rep.candidates = fetch_pairs(r.candidate_count);
-    rep.real_record_sizes.params = sizeof(ccdk_pipeline_cfg);
-    rep.real_record_sizes.query = 200; // kind byte + 24 doubles on the device
-    rep.real_record_sizes.interval = 36;
-    rep.real_record_sizes.pair_ints = 8;
+    // the API's own record sizes, as the reference reports them
+    // (pipeline.cpp:210-213); the device layouts are internal
+    rep.real_record_sizes.params = sizeof(PipelineConfig);
+    rep.real_record_sizes.query = sizeof(NarrowQuery);
+    rep.real_record_sizes.interval = sizeof(IntervalBox) + sizeof(ProcessResult);
+    rep.real_record_sizes.pair_ints = sizeof(CandidatePair);
     return rep;
 }
 
