@@ -148,11 +148,43 @@ def load_peaks():
 
 
 def load_traffic():
+    """ncu dram byte counts per launch / per step (profiles/traffic_r0N.json,
+    newest round first)."""
+    out = {}
+    for name in ("traffic_r01.json", "traffic_r02.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                out.update(json.load(f))
+        except Exception:
+            pass
+    return out
+
+
+def bench_config(workload, primitives):
+    """The `config` object of BOTH arms (identical keys and values, so the
+    driver can match the reference line to ours)."""
+    return {"workload": workload, "scene": WORKLOADS[workload], "primitives": primitives,
+            "l2": "ours: flushed (256 MiB memset) before every timed step; reference: CPU"}
+
+
+def host_info():
+    """CPU model and the compiler the reference CPU build used (BASELINE.md §2 'Host')."""
+    import subprocess
+    model = platform.processor() or platform.machine()
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
-            return json.load(f)
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cc = subprocess.run(["g++", "-dumpfullversion"], capture_output=True, text=True, timeout=10).stdout.strip()
+        compiler = f"g++ {cc} -std=gnu++20 -O3 -DNDEBUG (oracle/Makefile, unmodified reference sources)"
     except Exception:
-        return {}
+        compiler = "g++ -O3 (oracle/Makefile)"
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "compiler": compiler}
 
 
 def cpu_reference_step(scene, cfg_c, threads):
@@ -186,13 +218,12 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "scene": WORKLOADS[args.workload],
-                   "primitives": scene.primitive_count(), "broad_method": "sap"},
+        "config": bench_config(args.workload, scene.primitive_count()),
         "narrow_queries_per_s": rep.query_count / rep.t_np if rep.t_np > 0 else None,
         "candidates": rep.candidate_count, "toi": rep.toi,
         "stage_s": {"CB": rep.t_cb, "BP": rep.t_bp, "SO/CD": rep.t_socd, "NP": rep.t_np},
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
-                         "sample": sample, "cpu": platform.processor() or platform.machine()},
+                         "sample": sample, **host_info()},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -358,6 +389,9 @@ def run_ours(args):
     distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
     if distributed:
         import torch.distributed as dist
+        if world > 1:  # NCCL's INIT lines (nRanks, transports) go to stderr for the record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2112_06300_b200 import abi, ccdkit as ck, native, scenes
     from paper_2112_06300_b200.multigpu import RebalancedCcd, ShardedCcd
@@ -466,6 +500,7 @@ def run_ours(args):
                 cpu_ms, cpu_rep = cpu_reference_step(scene, cfg_ref.to_c(), threads)
                 cpu = {"value": cpu_ms, "unit": "ms", "cores": threads, "kind": "reference",
                        "sample": f"one full {args.workload} step, ccdkit_ref::ccd SAP threads={threads}",
+                       **host_info(),
                        "narrow_queries_per_s": cpu_rep.query_count / cpu_rep.t_np if cpu_rep.t_np else None,
                        "toi_matches": cpu_rep.toi == gtoi,
                        "candidates_match": cpu_rep.candidate_count == candidates}
@@ -511,6 +546,23 @@ def run_ours(args):
                       "algorithmic": f"B = 40k + 8C, k={k}, C={rep.candidate_count}",
                       "pair_tests": d["pair_tests"],
                       "pair_tests_per_s": d["pair_tests"] / (d["ms_sweep"] * 1e-3) if d["ms_sweep"] else None}
+    # HBM-bound prologue stages (north_star: "achieved HBM GB/s for the build,
+    # sort and sweep"), algorithmic bytes per SURVEY §8(d) over the device
+    # stage time of this step; `traffic` = ncu dram bytes of the same stage
+    def hbm_roofline(kernel, nbytes, stage_ms, traffic_key, formula):
+        gbs = nbytes / (stage_ms * 1e-3) / 1e9 if stage_ms > 0 else 0.0
+        return {"kernel": kernel, "bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": gbs / hbm_peak, "bytes": int(nbytes), "stage_ms": stage_ms,
+                "traffic": traffic.get(traffic_key), "algorithmic": formula}
+    roofline_build = hbm_roofline(
+        "k_build_boxes (K1)", 48.0 * scene.nv + 8.0 * scene.ne + 12.0 * scene.nf + 28.0 * k, d["ms_build"],
+        "build_bytes_per_step", f"B = 48nv + 8ne + 12nf + 28k, nv={scene.nv}, ne={scene.ne}, nf={scene.nf}")
+    roofline_sort = hbm_roofline(
+        "K2 axis + K3 key build, radix sort, permute + quantise", 16.0 * k, d["ms_sort"],
+        "sort_bytes_per_step", f"B = 16k (u32 key + u32 value, read + write once), k={k}")
+    roofline_pairsort = hbm_roofline(
+        "K6 candidate key radix sort", 16.0 * rep.candidate_count, d["ms_pairsort"],
+        "pairsort_bytes_per_step", f"B = 16C (u64 key read + write once), C={rep.candidate_count}")
     if c5:
         f5 = 339.0 * c5["evaluations"] + 96.0 * c5["split_actions"]
         a5 = f5 / (c5["ms"] * 1e-3) / 1e12 / world
@@ -523,11 +575,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "scene": WORKLOADS[args.workload], "primitives": k,
-                   "parallelism": f"sweep-range shards x{world}"
-                                  + (", candidates rebalanced by count (all_to_all)" if rebalance else "")
-                                  + ", allreduce(min)",
-                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "config": bench_config(args.workload, k),
+        "parallelism": f"sweep-range shards x{world}"
+                       + (", candidates rebalanced by count (all_to_all)" if rebalance else "")
+                       + ", allreduce(min)",
         "narrow_queries_per_s": queries / (narrow_ms * 1e-3) if narrow_ms > 0 else None,
         "candidates": candidates, "queries": queries, "toi": gtoi,
         "stage_ms": {kk: d[kk] for kk in ("ms_build", "ms_sort", "ms_sweep", "ms_pairsort",
@@ -543,7 +594,8 @@ def run_ours(args):
                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                          "api": "ResidentScene upload (pinned host buffers) + ccdk_ccd_resident step + "
                                 "global ToI; candidates stay on the device"},
-        "roofline": roofline, "roofline_sweep": roofline_sweep,
+        "roofline": roofline, "roofline_sweep": roofline_sweep, "roofline_build": roofline_build,
+        "roofline_sort": roofline_sort, "roofline_pairsort": roofline_pairsort,
         "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": int(d["kernel_launches"]) * args.steps,
         "wall_s_timed_region": wall,

@@ -240,8 +240,10 @@ CCDK_API int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_
              const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
              const ccdk_pipeline_cfg* cfg, ccdk_report* report);
 
-/* Candidate export for ccdk_ccd_into.  Called exactly once per step with the
- * final canonical candidate list in pinned host memory that is valid only
+/* Candidate export for ccdk_ccd_into.  Called twice per step: first with
+ * pairs == NULL and the final candidate count (the caller may allocate and
+ * fault in its destination while the list is still being copied), then with
+ * the final canonical candidate list in pinned host memory that is valid only
  * during the call: 16 bytes per pair, left id then right id, each id
  * {uint8 kind, 3 zero bytes, uint32 index} (= kind | index << 32 as a
  * little-endian u64, the in-memory layout of ccdkit::CandidatePair on
@@ -250,7 +252,7 @@ CCDK_API int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_
  * runs classify + narrow phase, so a caller's allocation and copy of the
  * list overlap the GPU; otherwise it runs on the calling thread before
  * ccdk_ccd_into returns.  Return 0, or nonzero to fail the call with
- * CCDK_OOM (e.g. the caller could not allocate). */
+ * CCDK_OOM (e.g. the caller could not allocate; no second call follows). */
 typedef int (*ccdk_pairs_sink)(void* user, const uint64_t* pairs, uint64_t n_pairs);
 
 /* ccd returning the candidate list through `sink` (the drop-in's

@@ -385,37 +385,69 @@ void export_begin(Ctx& c, const uint64_t* keys, uint64_t n, uint64_t nv, uint64_
 {
     PairExport& x = *c.exp;
     x.started = true;
+    x.n = n;
     if (!c.copy_stream)
         CCDK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
-    void* pin = c.pin_pairs.ensure(std::max<uint64_t>(16 * n, 16));
-    cudaEvent_t ready = c.events.get(EventPool::kExport), done = c.events.get(EventPool::kExport + 1);
-    if (n) {
-        uint64_t* ids = grow<uint64_t>(c.pair_ids, 2 * n);
-        launch_keys_to_ids(c, keys, n, c.last_nb, nullptr, nullptr, nv, ne, ids, 1);
-        CCDK_CUDA_CHECK(cudaEventRecord(ready, c.stream));
-        CCDK_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, ready, 0));
-        CCDK_CUDA_CHECK(cudaMemcpyAsync(pin, ids, 16 * n, cudaMemcpyDeviceToHost, c.copy_stream));
-    }
-    CCDK_CUDA_CHECK(cudaEventRecord(done, c.copy_stream));
+    x.pin = c.pin_pairs.ensure(std::max<uint64_t>(16 * n, 16));
+    if (n)
+        launch_keys_to_ids(c, keys, n, c.last_nb, nullptr, nullptr, nv, ne, grow<uint64_t>(c.pair_ids, 2 * n), 1);
+    x.pending = true;
+    cudaEvent_t done = c.events.get(EventPool::kExport + 1);
     const int device = c.device;
-    auto deliver = [&x, pin, n, done, device] {
+    auto deliver = [&x, done, device](std::shared_future<void> issued) {
+        // announce the count first: the caller allocates (and faults in) its
+        // destination while the copy is still in flight
+        x.sink_rc = x.sink(x.user, nullptr, x.n);
+        issued.wait();
+        if (x.sink_rc || x.aborted.load())
+            return;
         cudaSetDevice(device);
         const cudaError_t r = cudaEventSynchronize(done);
         if (r != cudaSuccess) {
             x.error = std::string("candidate export: ") + cudaGetErrorString(r);
             return;
         }
-        x.sink_rc = x.sink(x.user, static_cast<const uint64_t*>(pin), n);
+        x.sink_rc = x.sink(x.user, static_cast<const uint64_t*>(x.pin), x.n);
     };
-    if (async)
-        x.worker = std::thread(deliver);
-    else
-        deliver();
+    std::shared_future<void> issued = x.issued.get_future().share();
+    if (async) {
+        x.worker = std::thread(deliver, issued);
+    } else {
+        export_issue(c);
+        deliver(issued);
+    }
 }
+
+} // namespace
+
+void export_issue(Ctx& c)
+{
+    PairExport& x = *c.exp;
+    if (!x.pending)
+        return;
+    x.pending = false;
+    cudaEvent_t ready = c.events.get(EventPool::kExport), done = c.events.get(EventPool::kExport + 1);
+    try {
+        if (x.n) {
+            CCDK_CUDA_CHECK(cudaEventRecord(ready, c.stream));
+            CCDK_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, ready, 0));
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(x.pin, c.pair_ids.as<uint64_t>(), 16 * x.n, cudaMemcpyDeviceToHost,
+                                            c.copy_stream));
+        }
+        CCDK_CUDA_CHECK(cudaEventRecord(done, c.copy_stream));
+    } catch (...) {
+        x.issued.set_value();
+        throw;
+    }
+    x.issued.set_value();
+}
+
+namespace {
 
 void export_finish(Ctx& c)
 {
     PairExport& x = *c.exp;
+    export_issue(c); // no narrow phase ran (no candidates): issue now
     if (x.worker.joinable())
         x.worker.join();
     if (!x.error.empty())
@@ -1549,10 +1581,15 @@ int ccdk_ccd_into(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv
         PairExport x;
         x.sink = sink;
         x.user = user;
-        struct Scope { // never leave with the worker running
+        struct Scope { // never leave with the worker running or waiting
             Ctx& c;
             ~Scope()
             {
+                if (c.exp && c.exp->pending) {
+                    c.exp->pending = false;
+                    c.exp->aborted = true; // the worker must not deliver
+                    c.exp->issued.set_value();
+                }
                 if (c.exp && c.exp->worker.joinable())
                     c.exp->worker.join();
                 c.exp = nullptr;

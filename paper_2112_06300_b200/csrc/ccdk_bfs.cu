@@ -1046,6 +1046,8 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
                                                                         uint64_t(8) * c.num_sms));
     const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
 
+    if (c.exp && c.exp->pending)
+        export_issue(c); // candidate export D2H runs under the generations
     static const bool no_graph = std::getenv("CCDK_NO_GRAPH") != nullptr;
     if (!no_graph) {
         launch_generations(c, a, gen0_grid, gen_grid, fin_grid);

@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
+#include <atomic>
+#include <future>
 #include <string>
 #include <thread>
 #include <vector>
@@ -323,10 +325,19 @@ struct PairExport {
     ccdk_pairs_sink sink = nullptr;
     void* user = nullptr;
     bool started = false;
+    bool pending = false;  // converted on the device, D2H not yet issued
+    uint64_t n = 0;
+    void* pin = nullptr;
     int sink_rc = 0;
+    std::atomic<bool> aborted { false };
     std::string error;
+    std::promise<void> issued; // the worker waits for the D2H to be enqueued
     std::thread worker;
 };
+// Enqueue the pending export D2H (ccdk_api.cu).  The narrow phase calls it
+// right before its generation graph so the bulk copy never sits in front of
+// the small pre-narrow copies on the copy engine.
+void export_issue(Ctx& c);
 
 // ------------------------------------------------------------------ context
 

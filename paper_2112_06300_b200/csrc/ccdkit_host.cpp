@@ -17,10 +17,14 @@
 #include "ccdkit/pipeline.hpp"
 #include "ccdkit/scene.hpp"
 
+#include <sys/mman.h>
+
+#include <algorithm>
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <thread>
 #include <mutex>
 #include <stdexcept>
 
@@ -487,15 +491,54 @@ static_assert(sizeof(PrimitiveId) == 8 && offsetof(PrimitiveId, index) == 4 && s
 
 namespace {
 
+#ifdef MADV_POPULATE_WRITE
+constexpr int kPopulateWrite = MADV_POPULATE_WRITE;
+#else
+constexpr int kPopulateWrite = 23; // Linux 5.14+; older kernels reject it (EINVAL): a no-op hint
+#endif
+
 struct CandidateSink {
     std::vector<CandidatePair>* out;
     std::exception_ptr err;
 };
 
+// Fault in a fresh destination before the copy: 2 MB pages where the kernel
+// allows them (transparent huge pages in madvise mode) and the page tables
+// populated by several threads at once.  A 2M-candidate list is 34 MB; faulted
+// 4 KB at a time by the copy itself it costs more host time than the whole
+// device step.  Hints only: any failure leaves the ordinary fault path.
+void prefault(void* p, size_t bytes)
+{
+    constexpr uintptr_t kPage = 4096, kHuge = uintptr_t(2) << 20;
+    if (bytes < 4 * kHuge)
+        return;
+    const uintptr_t b = (reinterpret_cast<uintptr_t>(p) + kPage - 1) & ~(kPage - 1);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(kPage - 1);
+    madvise(reinterpret_cast<void*>(b), e - b, MADV_HUGEPAGE);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = static_cast<unsigned>(std::min<uintptr_t>({ 4u, std::max(1u, hw / 2), (e - b) / kHuge }));
+    const uintptr_t chunk = ((e - b) / nt + kHuge - 1) & ~(kHuge - 1);
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nt; ++t) {
+        const uintptr_t s = b + t * chunk, f = std::min(e, s + chunk);
+        if (s < f)
+            pool.emplace_back([s, f] { madvise(reinterpret_cast<void*>(s), f - s, kPopulateWrite); });
+    }
+    madvise(reinterpret_cast<void*>(b), std::min(e, b + chunk) - b, kPopulateWrite);
+    for (auto& th : pool)
+        th.join();
+}
+
 int candidate_sink(void* user, const uint64_t* pairs, uint64_t n)
 {
     auto* st = static_cast<CandidateSink*>(user);
     try {
+        if (!pairs) { // the count, while the copy is in flight: allocate and fault in
+            st->out->clear();
+            st->out->reserve(n);
+            prefault(st->out->data(), n * sizeof(CandidatePair));
+            return 0;
+        }
         const auto* p = reinterpret_cast<const CandidatePair*>(pairs);
         st->out->assign(p, p + n);
         return 0;

@@ -66,12 +66,39 @@ def sorted_run_lengths(min_corner: np.ndarray, max_corner: np.ndarray, axis: int
     return order, (end - p - 1).astype(np.uint64)
 
 
+def host_staged(group=None) -> bool:
+    """gloo moves host memory: device tensors are staged through the host
+    (the world-2-on-one-GPU tests; NCCL refuses two ranks on one device).
+    Under NCCL every collective runs on the device buffers directly."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
 def allreduce_min_toi(toi_tensor, group=None):
     """The single collective of the step: allreduce(min) of the global ToI
     (a 1-element float64 tensor, CUDA under NCCL or CPU under gloo)."""
     import torch.distributed as dist
+    if toi_tensor.is_cuda and host_staged(group):
+        t = toi_tensor.cpu()
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        toi_tensor.copy_(t)
+        return toi_tensor
     dist.all_reduce(toi_tensor, op=dist.ReduceOp.MIN, group=group)
     return toi_tensor
+
+
+def all_gather_counts(n: int, world: int, device, group=None):
+    """all_gather of one int64 per rank (the candidate counts)."""
+    import torch
+    import torch.distributed as dist
+    if host_staged(group):
+        out = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(out, torch.tensor([n], dtype=torch.int64), group=group)
+        return [int(x.item()) for x in out]
+    cnt = torch.tensor([n], dtype=torch.int64, device=device)
+    gathered = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(gathered, cnt, group=group)
+    return [int(c) for c in gathered.cpu().tolist()]  # one read-back for all N counts
 
 
 def bind_to_torch_stream(resident):
@@ -142,6 +169,11 @@ def rebalance_keys(keys, counts, rank: int, world: int, group=None):
     import torch
     import torch.distributed as dist
     send, recv = exchange_splits(counts, rank, world)
+    if keys.is_cuda and host_staged(group):
+        out = torch.empty(sum(recv), dtype=keys.dtype)
+        dist.all_to_all_single(out, keys[:sum(send)].cpu().contiguous(), output_split_sizes=recv,
+                               input_split_sizes=send, group=group)
+        return out.to(keys.device)
     out = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
     dist.all_to_all_single(out, keys[:sum(send)].contiguous(), output_split_sizes=recv,
                            input_split_sizes=send, group=group)
@@ -167,10 +199,7 @@ class RebalancedCcd:
         import torch
         import torch.distributed as dist
         n, nb, broad_ms = self.resident.broad(cfg, self.rank, self.world)
-        cnt = torch.tensor([n], dtype=torch.int64, device=self.dev)
-        gathered = torch.empty(self.world, dtype=torch.int64, device=self.dev)
-        dist.all_gather_into_tensor(gathered, cnt, group=self.group)
-        counts = [int(c) for c in gathered.cpu().tolist()]  # one read-back for all N counts
+        counts = all_gather_counts(n, self.world, self.dev, self.group)
         if self.keys.numel() < max(n, 1):
             self.keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
         self.resident.copy_keys(self.keys.data_ptr())

@@ -16,6 +16,8 @@ static double ms(Clock::time_point a, Clock::time_point b) { return std::chrono:
 static int noop_sink(void*, const uint64_t*, uint64_t) { return 0; }
 static int fill_sink(void* u, const uint64_t* p, uint64_t n)
 {
+    if (!p)
+        return 0;
     auto* v = static_cast<std::vector<ccdkit::CandidatePair>*>(u);
     const auto* c = reinterpret_cast<const ccdkit::CandidatePair*>(p);
     v->assign(c, c + n);
