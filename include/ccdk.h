@@ -147,7 +147,9 @@ CCDK_API int ccdk_abi_version(void);
 CCDK_API const char* ccdk_last_error(void);
 CCDK_API int ccdk_ctx_create(int device, ccdk_ctx** out);
 CCDK_API int ccdk_ctx_destroy(ccdk_ctx* ctx);
-/* Run all work of this context on `stream` (a cudaStream_t); NULL = own stream. */
+/* Run all work of this context on `stream` (a cudaStream_t); NULL = a private
+ * non-blocking stream of the context (the default: NOT ordered with any other
+ * stream).  To share the legacy default stream pass cudaStreamLegacy (0x1). */
 CCDK_API int ccdk_ctx_set_stream(ccdk_ctx* ctx, void* stream);
 CCDK_API int ccdk_ctx_synchronize(ccdk_ctx* ctx);
 /* Narrow-phase interval buffer capacity (intervals per generation buffer).

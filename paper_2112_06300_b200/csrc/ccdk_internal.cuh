@@ -398,6 +398,7 @@ struct Ctx {
     DevBuf all_keys, all_toi, all_flags;
     bool last_keys_all = false; // fetch_pairs reads all_keys (pipeline) or pair_keys_sorted (API)
 
+    PinnedBuf pin_scene;               // staging of pageable scene uploads
     // candidate export (ccdk_ccd_into)
     PairExport* exp = nullptr;
     DevBuf pair_ids;

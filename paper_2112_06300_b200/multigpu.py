@@ -12,10 +12,12 @@ the only exchange is the 8-byte allreduce(min) of the ToI, run on the device
 buffer the step wrote (NCCL over NVLink on GPUs, gloo in the CPU tests).
 
 Narrow-phase load balance: equal sweep work does not mean
-equal candidate counts, so RebalancedCcd splits the step at the candidate
-list: after the sweep, ranks all-gather their counts (N integers) and move
-pair keys with ONE all_to_all so that rank r narrow-phases the r-th equal
-slice of the rank-ordered concatenation of all candidates.  Every rank holds
+equal narrow work, so RebalancedCcd splits the step at the candidate list:
+after the sweep, ranks all-gather their counts (N integers) and move pair
+keys with ONE all_to_all so that rank r narrow-phases every N-th candidate
+(global index = r mod N) of the rank-ordered concatenation — interleaved,
+because per-query BFS cost is clustered along the canonical order (see
+rebalance_keys).  Every rank holds
 the replicated scene, so an 8-byte key is all a rank needs to gather the
 query's coordinates; per-query results are partition-independent
 (narrowphase.hpp:93-96), so the ToI is unchanged.
@@ -66,6 +68,9 @@ def sorted_run_lengths(min_corner: np.ndarray, max_corner: np.ndarray, axis: int
     return order, (end - p - 1).astype(np.uint64)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream, torch's stream 0
+
+
 def host_staged(group=None) -> bool:
     """gloo moves host memory: device tensors are staged through the host
     (the world-2-on-one-GPU tests; NCCL refuses two ranks on one device).
@@ -112,7 +117,11 @@ def bind_to_torch_stream(resident):
     all_to_all has not delivered yet."""
     import torch
     dev = torch.device(f"cuda:{resident.ctx.device}")
-    resident.ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    handle = torch.cuda.current_stream(dev).cuda_stream
+    # torch's default stream has handle 0, which ccdk_ctx_set_stream reads as
+    # "a private stream of your own" — the very unordered case this contract
+    # rules out; name it as the legacy default stream instead
+    resident.ctx.set_stream(handle or CUDA_STREAM_LEGACY)
     return dev
 
 
@@ -162,13 +171,46 @@ def exchange_splits(counts, rank: int, world: int):
     return send, recv
 
 
-def rebalance_keys(keys, counts, rank: int, world: int, group=None):
+def _residue_count(n: int, first: int, world: int) -> int:
+    """#{j in [0, n) : j = first (mod world)} for 0 <= first < world."""
+    return 0 if first >= n else (n - 1 - first) // world + 1
+
+
+def interleave_splits(counts, rank: int, world: int):
+    """all_to_all split sizes of the interleaved policy: the candidate with
+    global index g (rank-ordered concatenation) goes to rank g mod world."""
+    counts = [int(c) for c in counts]
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    off, n = int(offs[rank]), counts[rank]
+    send = [_residue_count(n, (d - off) % world, world) for d in range(world)]
+    recv = [_residue_count(counts[s], (rank - int(offs[s])) % world, world) for s in range(world)]
+    return send, recv
+
+
+def rebalance_keys(keys, counts, rank: int, world: int, group=None, policy: str = "interleave"):
     """Move pair keys (a 1-D int64 tensor holding this rank's counts[rank]
-    keys, any device) so each rank ends with its balanced slice; one
-    all_to_all_single (NCCL on GPUs, gloo on CPU)."""
+    keys, any device) to their narrow-phase owners with one all_to_all_single
+    (NCCL on GPUs, gloo on CPU).
+
+    policy "interleave" (default): global candidate g goes to rank g mod N.
+    Narrow-phase cost per query is heavy-tailed and spatially clustered (deep
+    BFS trees next to the contact front), and the canonical order keeps
+    neighbours together, so equal contiguous slices of it are NOT equal work:
+    measured on C4 at N = 8 (profiles/r02_predict_scaling_C4.json) the
+    heaviest contiguous slice took 4.5 ms of narrow phase against 0.34 ms for
+    the lightest.  Striding spreads every cluster over all ranks.
+    policy "contiguous": rank r takes the r-th equal slice."""
     import torch
     import torch.distributed as dist
-    send, recv = exchange_splits(counts, rank, world)
+    n = int(counts[rank])
+    if policy == "interleave":
+        send, recv = interleave_splits(counts, rank, world)
+        off = int(sum(int(c) for c in counts[:rank]))
+        # keys bound for rank d are j = (d - off) mod N, + N, + 2N, ... : one gather
+        perm = torch.cat([torch.arange((d - off) % world, n, world, device=keys.device) for d in range(world)])
+        keys = keys[:n][perm] if n else keys[:0]
+    else:
+        send, recv = exchange_splits(counts, rank, world)
     if keys.is_cuda and host_staged(group):
         out = torch.empty(sum(recv), dtype=keys.dtype)
         dist.all_to_all_single(out, keys[:sum(send)].cpu().contiguous(), output_split_sizes=recv,
@@ -185,12 +227,13 @@ class RebalancedCcd:
     count: sweep shard -> all_gather(counts) -> all_to_all(keys) -> classify +
     narrow on the balanced slice -> allreduce(min) of the ToI."""
 
-    def __init__(self, resident, rank: int, world: int, group=None):
+    def __init__(self, resident, rank: int, world: int, group=None, policy: str = "interleave"):
         import torch
         self.resident = resident
         self.rank = rank
         self.world = world
         self.group = group
+        self.policy = policy
         self.dev = bind_to_torch_stream(resident)
         self.toi = torch.full((1,), float("inf"), dtype=torch.float64, device=self.dev)
         self.keys = torch.empty(0, dtype=torch.int64, device=self.dev)
@@ -203,7 +246,7 @@ class RebalancedCcd:
         if self.keys.numel() < max(n, 1):
             self.keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
         self.resident.copy_keys(self.keys.data_ptr())
-        mine = rebalance_keys(self.keys, counts, self.rank, self.world, self.group)
+        mine = rebalance_keys(self.keys, counts, self.rank, self.world, self.group, self.policy)
         rep = self.resident.narrow_keys(cfg, mine.data_ptr(), mine.numel(), nb)
         self.resident.copy_toi_to(self.toi.data_ptr())
         allreduce_min_toi(self.toi, self.group)

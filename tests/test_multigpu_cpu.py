@@ -93,7 +93,7 @@ def test_shard_bounds_partition(count):
         assert int(run_len[lo:hi].sum()) <= total / count + int(run_len.max())
 
 
-def _rebalance_worker(rank, world, port, result_path):
+def _rebalance_worker(rank, world, port, result_path, policy="contiguous"):
     import torch
     import torch.distributed as dist
 
@@ -104,7 +104,7 @@ def _rebalance_worker(rank, world, port, result_path):
     counts = [37, 5] if world == 2 else [1] * world
     rng = np.random.default_rng(100 + rank)
     keys = torch.from_numpy(rng.integers(0, 1 << 40, counts[rank], dtype=np.int64))
-    mine = rebalance_keys(keys, counts, rank, world)
+    mine = rebalance_keys(keys, counts, rank, world, policy=policy)
     # what every rank holds, gathered for the check
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(sizes, torch.tensor([mine.numel()], dtype=torch.int64))
@@ -120,22 +120,41 @@ def _rebalance_worker(rank, world, port, result_path):
     if rank == 0:
         concat = np.concatenate([s[:c].numpy() for s, c in zip(src, counts)])
         held = [g[:int(n.item())].numpy() for g, n in zip(got, sizes)]
-        rngs = balanced_ranges(counts, world)
-        ok = all(np.array_equal(h, concat[lo:hi]) for h, (lo, hi) in zip(held, rngs))
+        if policy == "contiguous":
+            rngs = balanced_ranges(counts, world)
+            ok = all(np.array_equal(h, concat[lo:hi]) for h, (lo, hi) in zip(held, rngs))
+        else:  # rank r holds global indices r, r+N, r+2N, ... in order
+            ok = all(np.array_equal(h, concat[r::world]) for r, h in enumerate(held))
         ok = ok and max(len(h) for h in held) - min(len(h) for h in held) <= 1
         with open(result_path, "w") as f:
             f.write("ok" if ok else "bad")
     dist.destroy_process_group()
 
 
-def test_rebalance_keys_gloo_world2(tmp_path):
+@pytest.mark.parametrize("policy", ["interleave", "contiguous"])
+def test_rebalance_keys_gloo_world2(tmp_path, policy):
     """after the sweep, one all_to_all moves pair keys so each
-    rank holds an equal slice (within one) of the rank-ordered concatenation."""
+    rank holds an equal share (within one) of the rank-ordered concatenation:
+    every N-th candidate (interleave, the default) or a contiguous slice."""
     import torch.multiprocessing as mp
     out = tmp_path / "res.txt"
-    mp.start_processes(_rebalance_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True,
+    mp.start_processes(_rebalance_worker, args=(2, _free_port(), str(out), policy), nprocs=2, join=True,
                        start_method="spawn")
     assert out.read_text() == "ok"
+
+
+def test_interleave_splits_host():
+    from paper_2112_06300_b200.multigpu import interleave_splits
+    counts = [10, 3, 7, 0, 5]
+    world = 5
+    total = sum(counts)
+    sends = [interleave_splits(counts, r, world)[0] for r in range(world)]
+    recvs = [interleave_splits(counts, r, world)[1] for r in range(world)]
+    for r in range(world):
+        assert sum(sends[r]) == counts[r]
+        assert sum(recvs[r]) == len(range(r, total, world))
+        for s in range(world):
+            assert sends[s][r] == recvs[r][s]
 
 
 def test_exchange_splits_host():

@@ -7,8 +7,10 @@ timed with CUDA events on the context's stream, L2 flushed before each:
   sharded    ccdk_ccd_resident(cfg, r, N): replicated build + sort, the
              SweepRange shard's sweep, its candidates' classify + narrow
   rebalanced ccdk_broad_resident(cfg, r, N) on every rank, then the
-             rank-ordered concatenation of all keys is cut into N equal
-             slices and rank r's slice runs ccdk_ccd_keys_resident
+             rank-ordered concatenation of all keys is split N ways —
+             contiguous equal slices, or interleaved (global index = r mod N,
+             multigpu.rebalance_keys' default) — and rank r's share runs
+             ccdk_ccd_keys_resident
 
 The predicted N-GPU step is the max over ranks of each phase plus the
 collectives (all_gather of N counts, one all_to_all of 8-byte keys, one
@@ -85,21 +87,28 @@ def main():
                 keys.append(buf[:cnt].clone())
             allk = torch.cat(keys)
             total = allk.numel()
-            narrow = []
-            for r in range(n):
-                lo, hi = total * r // n, total * (r + 1) // n
-                sl = allk[lo:hi].contiguous()
-                ms, rep = timed(lambda sl=sl: res.narrow_keys(cfg, sl.data_ptr(), sl.numel(), nb))
-                narrow.append({"rank": r, "narrow_step_ms": ms, "queries": rep.query_count})
-            moved = sum(abs(b["candidates"] - total // n) for b in broad) // 2
-            exch_ms = 3 * coll_us * 1e-3 + 8.0 * moved / (nvlink_gbs * 1e9) * 1e3
-            pred_sh = max(x["step_ms"] for x in sharded) + coll_us * 1e-3
-            pred_rb = max(b["broad_ms"] for b in broad) + max(x["narrow_step_ms"] for x in narrow) + exch_ms
+            narrow = {"contiguous": [], "interleave": []}
+            for policy in narrow:
+                for r in range(n):
+                    if policy == "contiguous":
+                        sl = allk[total * r // n:total * (r + 1) // n].contiguous()
+                    else:
+                        sl = allk[r::n].contiguous()
+                    ms, rep = timed(lambda sl=sl: res.narrow_keys(cfg, sl.data_ptr(), sl.numel(), nb))
+                    narrow[policy].append({"rank": r, "narrow_step_ms": ms, "queries": rep.query_count,
+                                           "generations": rep.device["generations"]})
+            moved = {"contiguous": sum(abs(b["candidates"] - total // n) for b in broad) // 2,
+                     "interleave": total - total // n}
+            exch = {p: 3 * coll_us * 1e-3 + 8.0 * m / (nvlink_gbs * 1e9) * 1e3 for p, m in moved.items()}
+            pred = {"sharded": max(x["step_ms"] for x in sharded) + coll_us * 1e-3}
+            for policy in narrow:
+                pred[f"rebalanced_{policy}"] = (max(b["broad_ms"] for b in broad)
+                                                + max(x["narrow_step_ms"] for x in narrow[policy]) + exch[policy])
             result["per_n"][n] = {
                 "sharded": sharded, "rebalanced_broad": broad, "rebalanced_narrow": narrow,
-                "keys_moved": moved, "collectives_ms_est": exch_ms,
-                "predicted_step_ms": {"sharded": pred_sh, "rebalanced": pred_rb},
-                "predicted_speedup_vs_n1": {"sharded": ms1 / pred_sh, "rebalanced": ms1 / pred_rb},
+                "keys_moved": moved, "collectives_ms_est": exch,
+                "predicted_step_ms": pred,
+                "predicted_speedup_vs_n1": {k: ms1 / v for k, v in pred.items()},
             }
     txt = json.dumps(result, indent=1)
     if args.out:
