@@ -545,7 +545,9 @@ def run_ours(args):
                       "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                       "algorithmic": f"B = 40k + 8C, k={k}, C={rep.candidate_count}",
                       "pair_tests": d["pair_tests"],
-                      "pair_tests_per_s": d["pair_tests"] / (d["ms_sweep"] * 1e-3) if d["ms_sweep"] else None}
+                      "pair_tests_per_s": d["pair_tests"] / (d["ms_sweep"] * 1e-3) if d["ms_sweep"] else None,
+                      "sweep": (f"slab mode: {d['sweep_slabs']} slabs, {d['sweep_entries']} entries (boxes incl. "
+                                f"copies in further slabs)") if d.get("sweep_slabs") else "1-D sweep"}
     # HBM-bound prologue stages (north_star: "achieved HBM GB/s for the build,
     # sort and sweep"), algorithmic bytes per SURVEY §8(d) over the device
     # stage time of this step; `traffic` = ncu dram bytes of the same stage

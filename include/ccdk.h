@@ -138,6 +138,8 @@ typedef struct {
     double ms_build, ms_sort, ms_sweep, ms_pairsort, ms_classify, ms_narrow, ms_total;
     uint64_t kernel_launches; /* own (non-CUB) kernels launched by this step */
     uint64_t broad_batches;   /* BatchTrace::broad_batches */
+    uint64_t sweep_slabs;     /* slab-mode sweep: slab count (0 = 1-D sweep) */
+    uint64_t sweep_entries;   /* slab-mode sweep: boxes incl. their copies in further slabs */
 } ccdk_report;
 
 typedef struct ccdk_ctx ccdk_ctx;

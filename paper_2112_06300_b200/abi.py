@@ -54,7 +54,8 @@ class Report(C.Structure):
                 ("ms_build", C.c_double), ("ms_sort", C.c_double), ("ms_sweep", C.c_double),
                 ("ms_pairsort", C.c_double), ("ms_classify", C.c_double),
                 ("ms_narrow", C.c_double), ("ms_total", C.c_double),
-                ("kernel_launches", C.c_uint64), ("broad_batches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("broad_batches", C.c_uint64),
+                ("sweep_slabs", C.c_uint64), ("sweep_entries", C.c_uint64)]
 
 
 def narrow_cfg(delta=1e-6, min_separation=0.0, t_max=1.0, max_splits=1 << 20,

@@ -409,7 +409,8 @@ def _report(r: abi.Report, pairs) -> CcdReport:
     dev = {k: getattr(r, k) for k, _ in abi.Report._fields_ if k.startswith("ms_")}
     dev.update(vf_count=r.vf_count, pair_tests=r.pair_tests, total_splits=r.total_splits,
                peak_queue=r.peak_queue, evaluations=r.evaluations, split_actions=r.split_actions,
-               generations=r.generations, axis=r.axis, kernel_launches=r.kernel_launches)
+               generations=r.generations, axis=r.axis, kernel_launches=r.kernel_launches,
+               sweep_slabs=r.sweep_slabs, sweep_entries=r.sweep_entries)
     return CcdReport(ToiResult(r.toi, bool(r.tolerance_hit), bool(r.zero_toi_diagnostic)),
                      int(r.candidate_count), int(r.query_count), int(r.batch_count),
                      {"CB": r.t_cb, "BP": r.t_bp, "SO/CD": r.t_socd, "NP": r.t_np},

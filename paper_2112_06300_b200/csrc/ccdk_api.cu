@@ -552,6 +552,7 @@ struct BatchRun {
     uint64_t peak_bytes = 0, base_bytes = 0;
     float ms_sort = 0, ms_sweep = 0, ms_pairsort = 0, ms_classify = 0, ms_narrow = 0;
     int axis = 0;
+    uint64_t slabs = 0, slab_entries = 0;
 
     // broad_batch (pipeline.cpp:140-174): halve the sweep range while the
     // candidates exceed the budget's pair capacity
@@ -577,6 +578,8 @@ struct BatchRun {
         ms_sweep += bo.ms_sweep;
         ms_pairsort += bo.ms_pairsort;
         axis = bo.axis;
+        slabs = bo.slab_count;
+        slab_entries = bo.slab_entries;
         if (shard_count > 1) { // this shard's slice of sorted left positions
             begin = bo.range_lo;
             end = bo.range_hi;
@@ -797,6 +800,8 @@ void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_
     rep.ms_total = ms_total;
     rep.kernel_launches = 1 + run.launches;
     rep.broad_batches = run.broad_batches;
+    rep.sweep_slabs = run.slabs;
+    rep.sweep_entries = run.slab_entries;
     rep.t_cb = ms_build * 1e-3;
     rep.t_bp = (run.ms_sort + run.ms_sweep + run.ms_pairsort) * 1e-3;
     rep.t_socd = run.ms_classify * 1e-3;

@@ -463,6 +463,10 @@ struct SweepArgs {
     unsigned long long* n_pairs;
     const Seg* segs;
     const unsigned long long* n_heavy;
+    // slab mode: entry's slab and its box's first slab; a pair is emitted only
+    // in its canonical slab max(first_p, first_q)
+    const uint32_t* slab;
+    const uint32_t* slab_first;
 };
 
 // keep_pair (broadphase.cpp:12-20) on vertex triples: the count of present
@@ -547,6 +551,8 @@ __device__ __forceinline__ void filter_hits(const SweepArgs& a, unsigned long lo
     const unsigned long long q = p + (h ? hits[lane] : 0u);
     // the quantised pass is a superset: the exact fp32 test decides
     h = h && box_hit(mb, a.sbox[q]);
+    if (a.slab) // slab mode: only the canonical slab of the pair emits it
+        h = h && max(a.slab_first[p], a.slab_first[q]) == a.slab[p];
     const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
     emit(a, h && keep_pair(mv, ov) && bf_ok(a, p, q), mv.w, ov.w);
 }
@@ -675,6 +681,160 @@ __global__ void __launch_bounds__(kRowsTB) k_sweep_heavy(SweepArgs a)
     }
 }
 
+// ---- K5' slab mode.  The candidate set is a property of the boxes alone
+// (closed overlap on all three axes + keep_pair, broadphase.cpp:12-20, 69-127),
+// not of the sweep that enumerates it, so any exact enumeration yields it.  A
+// 1-D sweep along the max-variance axis a tests every pair whose intervals
+// overlap on a: on a 410 x 410 cloth that is ~2,700 boxes per window (2.7e9
+// tests at C4), 97% of which miss on another axis.  Slab mode cuts space along
+// a second axis b into S slabs about twice the mean box extent wide, inserts
+// each box into every slab its b-interval touches, and sweeps every slab along
+// a exactly like K5: a window now holds only the boxes of one slab.  The slab
+// map s(x) = clamp(floor((x - lo) * inv_w)) is the same fp32 sequence for every
+// box, hence monotone, so two boxes that overlap on b both appear in slab
+// max(s(min_i), s(min_j)) — the first slab of the intersection of their slab
+// ranges — and the sweep emits a pair only there: exactly once.  Used for the
+// full-range broad phase (ccd's default step, stq/sap/bf without StqStats or
+// SweepRange); StqStats, SweepRange slices, budget halving and multi-GPU shards
+// keep the 1-D sweep whose positions they are defined on.
+struct SlabParams {
+    float lo, inv_w;
+    unsigned S;
+    int side; // 0: b = (a+1)%3 (sbox.x/.y), 1: b = (a+2)%3 (sbox.z/.w)
+    int ok;
+};
+constexpr unsigned kMaxSlabs = 65535; // slab ids sort on 16 bits
+
+__device__ __forceinline__ unsigned slab_of(const SlabParams& P, float x)
+{
+    const float f = floorf(__fmul_rn(__fsub_rn(x, P.lo), P.inv_w));
+    return f <= 0.0f ? 0u : f >= static_cast<float>(P.S - 1) ? P.S - 1 : static_cast<unsigned>(f);
+}
+
+// sums of the box extents along the two non-sweep axes (sorted boxes)
+__global__ void k_slab_stats(const float4* sbox, unsigned long long k, double* sums)
+{
+    double e1 = 0.0, e2 = 0.0;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < k;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const float4 b = sbox[i];
+        e1 += static_cast<double>(b.y) - static_cast<double>(b.x);
+        e2 += static_cast<double>(b.w) - static_cast<double>(b.z);
+    }
+    for (int o = 16; o; o >>= 1) {
+        e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sums[0], e1);
+        atomicAdd(&sums[1], e2);
+    }
+}
+
+// slab axis = the wider of the two non-sweep axes; width = 2 x its mean box
+// extent (at least ext / kMaxSlabs); ok = finite bounds and >= 2 slabs
+__global__ void k_slab_params(const unsigned* qb, const int* axis, const double* sums, unsigned long long k,
+                              SlabParams* P)
+{
+    const int a = *axis, a1 = (a + 1) % 3, a2 = (a + 2) % 3;
+    const float lo1 = ord2f(qb[a1]), hi1 = ord2f(qb[3 + a1]);
+    const float lo2 = ord2f(qb[a2]), hi2 = ord2f(qb[3 + a2]);
+    const double ext1 = static_cast<double>(hi1) - lo1, ext2 = static_cast<double>(hi2) - lo2;
+    const int side = ext2 > ext1 ? 1 : 0;
+    const float lo = side ? lo2 : lo1;
+    const double ext = side ? ext2 : ext1;
+    const double mean = sums[side] / static_cast<double>(k);
+    SlabParams p { lo, 0.0f, 1u, side, 0 };
+    if (isfinite(lo1) && isfinite(hi1) && isfinite(lo2) && isfinite(hi2) && ext > 0.0) {
+        const double w = fmax(2.0 * mean, ext / kMaxSlabs);
+        const double S = ceil(ext / w);
+        if (S >= 2.0 && w > 0.0) {
+            p.S = static_cast<unsigned>(fmin(S, static_cast<double>(kMaxSlabs)));
+            p.inv_w = static_cast<float>(1.0 / w);
+            p.ok = isfinite(p.inv_w) && p.inv_w > 0.0f;
+        }
+    }
+    *P = p;
+}
+
+__global__ void k_slab_count(const float4* sbox, unsigned long long k, const SlabParams* Pp, uint32_t* cnt)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (p >= k)
+        return;
+    const SlabParams P = *Pp;
+    const float4 b = sbox[p];
+    const float mn = P.side ? b.z : b.x, mx = P.side ? b.w : b.y;
+    cnt[p] = slab_of(P, mx) - slab_of(P, mn) + 1;
+}
+
+// entries in sorted-position order: (slab, position) for every slab a box touches
+__global__ void k_slab_emit(const float4* sbox, unsigned long long k, const SlabParams* Pp, const uint32_t* off,
+                            uint32_t* keys, uint32_t* vals)
+{
+    const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (p >= k)
+        return;
+    const SlabParams P = *Pp;
+    const float4 b = sbox[p];
+    const unsigned s0 = slab_of(P, P.side ? b.z : b.x), s1 = slab_of(P, P.side ? b.w : b.y);
+    uint32_t o = off[p];
+    for (unsigned s = s0; s <= s1; ++s, ++o) {
+        keys[o] = s;
+        vals[o] = static_cast<uint32_t>(p);
+    }
+}
+
+// slab-major SoA (the stable sort keeps each slab's entries in min-a order),
+// each entry's slab and its box's first slab, per-slab segment ends
+__global__ void k_slab_gather(const uint32_t* keys, const uint32_t* vals, unsigned long long E,
+                              const SlabParams* Pp, const float* smin_a, const float* smax_a, const float4* sbox,
+                              const uint4* svid, const uint2* sq, float* emin_a, float* emax_a, float4* ebox,
+                              uint4* evid, uint2* equant, uint32_t* eslab, uint32_t* efirst, uint32_t* slab_end)
+{
+    const unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (e >= E)
+        return;
+    const SlabParams P = *Pp;
+    const uint32_t p = vals[e], s = keys[e];
+    const float4 b = sbox[p];
+    emin_a[e] = smin_a[p];
+    emax_a[e] = smax_a[p];
+    ebox[e] = b;
+    evid[e] = svid[p];
+    equant[e] = sq[p];
+    eslab[e] = s;
+    efirst[e] = slab_of(P, P.side ? b.z : b.x);
+    if (e + 1 == E || keys[e + 1] != s)
+        slab_end[s] = static_cast<uint32_t>(e + 1);
+}
+
+// K4 per entry: the window ends at the first entry of the same slab whose
+// min-a exceeds this entry's max-a
+__global__ void k_slab_run_ends(const float* emin_a, const float* emax_a, const uint32_t* eslab,
+                                const uint32_t* slab_end, unsigned long long E, uint32_t* run_end,
+                                unsigned long long* pair_tests)
+{
+    const unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    unsigned long long len = 0;
+    if (e < E) {
+        const float reach = emax_a[e];
+        unsigned long long a = e + 1, b = slab_end[eslab[e]];
+        while (a < b) {
+            const unsigned long long m = (a + b) >> 1;
+            if (emin_a[m] <= reach)
+                a = m + 1;
+            else
+                b = m;
+        }
+        run_end[e] = static_cast<uint32_t>(a);
+        len = a - e - 1;
+    }
+    const unsigned long long s = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(len));
+    if ((threadIdx.x & 31) == 0 && s)
+        atomicAdd(pair_tests, s);
+}
+
 // ---- stats: StqStats::round_sizes[r] = #{i : run_len(i) >= r+1}
 
 __global__ void k_run_hist(const unsigned long long* run_len, unsigned long long k,
@@ -787,28 +947,105 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         lo = std::min<uint64_t>(in.range_begin, k - 1);
         hi = std::min<uint64_t>(in.range_end, k - 1);
     }
-    uint32_t* run_end = grow<uint32_t>(c.run_end, k);
-    const bool need_len = in.want_rounds || in.shard_count > 1;
-    unsigned long long* run_len = need_len ? grow<unsigned long long>(c.prefix, 2 * k) : nullptr;
-    k_run_ends<<<grid_for(k, 256), 256, 0, s>>>(smin_a, smax_a, k, lo, hi, run_end, run_len,
-                                                 &ctr->pair_tests);
-    CCDK_LAUNCH_CHECK();
+    // rows of the sweep: the k sorted boxes, or in slab mode the E slab entries
+    uint64_t rows = k;
+    const float* w_min = smin_a;
+    const float* w_max = smax_a;
+    const float4* w_box = sbox;
+    const uint4* w_vid = svid;
+    const uint2* w_q = sq;
+    const uint32_t* w_slab = nullptr;
+    const uint32_t* w_first = nullptr;
     unsigned long long* d_range = &ctr->misc[0]; // misc[0..1]
-    if (in.shard_count > 1) {
-        unsigned long long* incl = run_len + k;
+    uint32_t* run_end = nullptr;
+    static const bool slab_env_off = std::getenv("CCDK_SLAB") && std::getenv("CCDK_SLAB")[0] == '0';
+    const bool slab_try = !bf && !slab_env_off && lo == 0 && hi == k - 1 && in.shard_count == 1
+        && !in.want_rounds && k < (uint64_t(1) << 30);
+    if (slab_try) {
+        char* par = static_cast<char*>(c.slab_par.ensure(64));
+        double* sums = reinterpret_cast<double*>(par);
+        SlabParams* P = reinterpret_cast<SlabParams*>(par + 16);
+        CCDK_CUDA_CHECK(cudaMemsetAsync(sums, 0, 16, s));
+        k_slab_stats<<<kRedBlocks, kRedThreads, 0, s>>>(sbox, k, sums);
+        k_slab_params<<<1, 1, 0, s>>>(qb, d_axis, sums, k, P);
+        uint32_t* cnt = grow<uint32_t>(c.slab_cnt, 2 * k);
+        uint32_t* eoff = cnt + k;
+        k_slab_count<<<grid_for(k, 256), 256, 0, s>>>(sbox, k, P, cnt);
+        CCDK_LAUNCH_CHECK();
         cub_call(c, [&](void* t, size_t& b) {
-            return cub::DeviceScan::InclusiveSum(t, b, run_len, incl, static_cast<int64_t>(k), s);
+            return cub::DeviceScan::ExclusiveSum(t, b, cnt, eoff, static_cast<int64_t>(k), s);
         });
-        k_shard_range<<<1, 32, 0, s>>>(incl, lo, hi, in.shard_rank, in.shard_count, d_range);
-    } else {
-        k_full_range<<<1, 1, 0, s>>>(lo, hi, d_range);
+        uint32_t tail[2];
+        SlabParams hp {};
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[0], eoff + k - 1, 4, cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[1], cnt + k - 1, 4, cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&hp, P, sizeof hp, cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+        const uint64_t E = static_cast<uint64_t>(tail[0]) + tail[1];
+        // copies of wide boxes multiply the entries; beyond 4 k the 1-D sweep wins
+        if (hp.ok && E <= 4 * k) {
+            uint32_t* ek = grow<uint32_t>(c.slab_keys, 2 * E);
+            uint32_t* ev_ = grow<uint32_t>(c.slab_vals, 2 * E);
+            k_slab_emit<<<grid_for(k, 256), 256, 0, s>>>(sbox, k, P, eoff, ek, ev_);
+            CCDK_LAUNCH_CHECK();
+            cub_call(c, [&](void* t, size_t& b) { // stable: each slab stays in min-a order
+                return cub::DeviceRadixSort::SortPairs(t, b, ek, ek + E, ev_, ev_ + E, static_cast<int64_t>(E),
+                                                       0, 16, s);
+            });
+            float* emin = grow<float>(c.emin_a, E);
+            float* emax = grow<float>(c.emax_a, E);
+            float4* ebox = grow<float4>(c.ebox, E);
+            uint4* evid = grow<uint4>(c.evid, E);
+            uint2* eq = grow<uint2>(c.equant, E);
+            uint32_t* eslab = grow<uint32_t>(c.eslab, 2 * E);
+            uint32_t* efirst = eslab + E;
+            uint32_t* slab_end = grow<uint32_t>(c.slab_end, hp.S);
+            k_slab_gather<<<grid_for(E, 256), 256, 0, s>>>(ek + E, ev_ + E, E, P, smin_a, smax_a, sbox, svid, sq,
+                                                            emin, emax, ebox, evid, eq, eslab, efirst, slab_end);
+            run_end = grow<uint32_t>(c.run_end, E);
+            k_slab_run_ends<<<grid_for(E, 256), 256, 0, s>>>(emin, emax, eslab, slab_end, E, run_end,
+                                                              &ctr->pair_tests);
+            k_full_range<<<1, 1, 0, s>>>(0, E, d_range);
+            CCDK_LAUNCH_CHECK();
+            rows = E;
+            lo = 0;
+            hi = E;
+            w_min = emin;
+            w_max = emax;
+            w_box = ebox;
+            w_vid = evid;
+            w_q = eq;
+            w_slab = eslab;
+            w_first = efirst;
+            out.slab_mode = true;
+            out.slab_count = hp.S;
+            out.slab_entries = E;
+        }
     }
-    CCDK_LAUNCH_CHECK();
-    uint32_t* nseg = grow<uint32_t>(c.seg_off, 2 * k);
-    uint32_t* off = nseg + k;
-    k_heavy_count<<<grid_for(k, 256), 256, 0, s>>>(run_end, d_range, k, nseg);
+    const bool need_len = in.want_rounds || in.shard_count > 1;
+    unsigned long long* run_len = nullptr;
+    if (!out.slab_mode) {
+        run_end = grow<uint32_t>(c.run_end, k);
+        run_len = need_len ? grow<unsigned long long>(c.prefix, 2 * k) : nullptr;
+        k_run_ends<<<grid_for(k, 256), 256, 0, s>>>(smin_a, smax_a, k, lo, hi, run_end, run_len,
+                                                     &ctr->pair_tests);
+        CCDK_LAUNCH_CHECK();
+        if (in.shard_count > 1) {
+            unsigned long long* incl = run_len + k;
+            cub_call(c, [&](void* t, size_t& b) {
+                return cub::DeviceScan::InclusiveSum(t, b, run_len, incl, static_cast<int64_t>(k), s);
+            });
+            k_shard_range<<<1, 32, 0, s>>>(incl, lo, hi, in.shard_rank, in.shard_count, d_range);
+        } else {
+            k_full_range<<<1, 1, 0, s>>>(lo, hi, d_range);
+        }
+        CCDK_LAUNCH_CHECK();
+    }
+    uint32_t* nseg = grow<uint32_t>(c.seg_off, 2 * rows);
+    uint32_t* off = nseg + rows;
+    k_heavy_count<<<grid_for(rows, 256), 256, 0, s>>>(run_end, d_range, rows, nseg);
     cub_call(c, [&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, nseg, off, static_cast<int64_t>(k), s);
+        return cub::DeviceScan::ExclusiveSum(t, b, nseg, off, static_cast<int64_t>(rows), s);
     });
     // segments total <= sum over rows of ceil(k / kSeg); grow on demand below
     uint64_t seg_cap = std::max<uint64_t>(c.segs.cap / sizeof(Seg), 1024);
@@ -831,8 +1068,8 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     {
         // total heavy segments = off[k-1] + nseg[k-1]
         uint32_t tail[2];
-        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[0], off + k - 1, 4, cudaMemcpyDeviceToHost, s));
-        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[1], nseg + k - 1, 4, cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[0], off + rows - 1, 4, cudaMemcpyDeviceToHost, s));
+        CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[1], nseg + rows - 1, 4, cudaMemcpyDeviceToHost, s));
         read_ctr();
         const uint64_t total = static_cast<uint64_t>(tail[0]) + tail[1];
         if (total > seg_cap) {
@@ -860,7 +1097,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
             CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
         }
     }
-    k_heavy_gen<<<grid_for(k, 256), 256, 0, s>>>(run_end, nseg, off, k, segs, &ctr->n_heavy);
+    k_heavy_gen<<<grid_for(rows, 256), 256, 0, s>>>(run_end, nseg, off, rows, segs, &ctr->n_heavy);
     CCDK_LAUNCH_CHECK();
 
     // K5 sweep (re-run once with a larger buffer if the candidate count overflows)
@@ -873,16 +1110,18 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         unsigned long long* keys = grow<unsigned long long>(c.pair_keys, c.pair_capacity);
         CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->n_pairs, 0, 8, s));
         SweepArgs sa {};
-        sa.smin_a = smin_a;
-        sa.smax_a = smax_a;
-        sa.sbox = sbox;
-        sa.sq = sq;
-        sa.svid = svid;
+        sa.smin_a = w_min;
+        sa.smax_a = w_max;
+        sa.sbox = w_box;
+        sa.sq = w_q;
+        sa.svid = w_vid;
+        sa.slab = w_slab;
+        sa.slab_first = w_first;
         sa.sraw = sraw;
         sa.run_end = run_end;
         sa.range = d_range;
         sa.row0 = lo;
-        sa.k = k;
+        sa.k = rows;
         sa.nb = nb;
         sa.bf = bf;
         sa.bf_lo = in.range_begin;

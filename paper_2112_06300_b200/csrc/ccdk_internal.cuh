@@ -256,6 +256,8 @@ struct BroadOut {
     bool axis_near_tie = false; // tree-summed variances within the error bound of a tie
     bool axis_serial = false;   // ... and the reference's serial order decided the axis
     float ms_axis_sort = 0, ms_sweep = 0, ms_pairsort = 0;
+    bool slab_mode = false;     // the sweep ran per slab (K5'); entries = boxes incl. slab copies
+    uint64_t slab_count = 0, slab_entries = 0;
 };
 // General broad phase over SoA boxes whose slot order is owner order (rank =
 // slot) or, with owner arrays, an arbitrary box list.
@@ -361,6 +363,11 @@ struct Ctx {
     DevBuf squant;                     // sorted quantised filter boxes (uint2)
     DevBuf qbounds;                    // quantisation bounds (ordered u32 min[3], max[3])
     DevBuf run_end, seg_off, segs, prefix;
+    // slab-mode sweep (K5'): per-box slab counts/offsets, (slab, position)
+    // entries before/after the stable slab sort, the slab-major SoA, per-slab
+    // segment ends, parameters
+    DevBuf slab_cnt, slab_keys, slab_vals, slab_end, slab_par;
+    DevBuf emin_a, emax_a, ebox, evid, equant, eslab;
     DevBuf pair_keys, pair_keys_sorted;
     DevBuf rounds;
     DevBuf cub_tmp;
