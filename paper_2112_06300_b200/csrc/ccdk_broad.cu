@@ -403,17 +403,17 @@ __global__ void k_full_range(unsigned long long lo, unsigned long long hi, unsig
 }
 
 __global__ void k_heavy_count(const uint32_t* run_end, const unsigned long long* range,
-                              unsigned long long k, uint32_t* nseg)
+                              unsigned long long k, uint32_t* nseg, uint32_t cap, uint32_t seg)
 {
     const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (p >= k)
         return;
     uint32_t n = 0;
     if (p >= range[0] && p < range[1]) {
-        const unsigned long long start = p + 1 + kCap;
+        const unsigned long long start = p + 1 + cap;
         const unsigned long long end = run_end[p];
         if (end > start)
-            n = static_cast<uint32_t>((end - start + kSeg - 1) / kSeg);
+            n = static_cast<uint32_t>((end - start + seg - 1) / seg);
     }
     nseg[p] = n;
 }
@@ -423,7 +423,8 @@ struct Seg {
 };
 
 __global__ void k_heavy_gen(const uint32_t* run_end, const uint32_t* nseg, const uint32_t* off,
-                            unsigned long long k, Seg* segs, unsigned long long* n_heavy)
+                            unsigned long long k, Seg* segs, unsigned long long* n_heavy, uint32_t cap,
+                            uint32_t seg)
 {
     const unsigned long long p = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (p >= k)
@@ -433,11 +434,11 @@ __global__ void k_heavy_gen(const uint32_t* run_end, const uint32_t* nseg, const
         *n_heavy = static_cast<unsigned long long>(off[p]) + n;
     if (!n)
         return;
-    const uint32_t start = static_cast<uint32_t>(p + 1 + kCap);
+    const uint32_t start = static_cast<uint32_t>(p + 1 + cap);
     const uint32_t end = run_end[p];
     for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t jb = start + i * kSeg;
-        const uint32_t je = min(end, jb + kSeg);
+        const uint32_t jb = start + i * seg;
+        const uint32_t je = min(end, jb + seg);
         segs[off[p] + i] = { static_cast<uint32_t>(p), jb, je, 0 };
     }
 }
@@ -463,6 +464,8 @@ struct SweepArgs {
     unsigned long long* n_pairs;
     const Seg* segs;
     const unsigned long long* n_heavy;
+    unsigned long long short_len; // rows with windows <= this go to k_sweep_short (0: none)
+    unsigned long long row_cap;   // per-row window handled by k_sweep_rows; the rest: heavy segments
     // slab mode: entry's slab and its box's first slab; a pair is emitted only
     // in its canonical slab max(first_p, first_q)
     const uint32_t* slab;
@@ -491,24 +494,57 @@ __device__ __forceinline__ bool box_hit(float4 m, float4 o)
     return o.x <= m.y && m.x <= o.y && o.z <= m.w && m.z <= o.w;
 }
 
-__device__ __forceinline__ void emit(const SweepArgs& a, bool keep, uint32_t ra, uint32_t rb)
+// Kept pairs of a warp wait in shared memory and go out 32 at a time with one
+// warp-aggregated atomic.  Most quantised hits fail the exact test or
+// keep_pair (neighbouring triangles share vertices; a floor face pairs only
+// with vertices), so emitting per drain would pay the atomic's round trip
+// for a handful of keys.
+constexpr int kOutBuf = 64;
+struct WarpOut {
+    unsigned long long* buf; // kOutBuf keys, per warp in shared memory
+    unsigned n;              // warp-uniform
+};
+
+__device__ __forceinline__ void out_flush(const SweepArgs& a, WarpOut& o, unsigned cnt, unsigned lane)
 {
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (!mask)
-        return;
-    const unsigned lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
     unsigned long long base = 0;
-    if (lane == static_cast<unsigned>(leader))
-        base = atomicAdd(a.n_pairs, static_cast<unsigned long long>(__popc(mask)));
-    base = __shfl_sync(0xffffffffu, base, leader);
+    if (lane == 0)
+        base = atomicAdd(a.n_pairs, static_cast<unsigned long long>(cnt));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < cnt && base + lane < a.cap)
+        a.keys[base + lane] = o.buf[lane];
+}
+
+// append the lanes' kept pairs; flush whenever 32 are waiting
+__device__ __forceinline__ void out_push(const SweepArgs& a, WarpOut& o, bool keep, uint32_t ra, uint32_t rb,
+                                         unsigned lane)
+{
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m)
+        return;
     if (keep) {
-        const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1));
-        if (slot < a.cap) {
-            const uint32_t lo = min(ra, rb), hi = max(ra, rb);
-            a.keys[slot] = (static_cast<unsigned long long>(lo) << a.nb) | hi;
-        }
+        const uint32_t lo = min(ra, rb), hi = max(ra, rb);
+        o.buf[o.n + __popc(m & ((1u << lane) - 1))] = (static_cast<unsigned long long>(lo) << a.nb) | hi;
     }
+    o.n += __popc(m);
+    __syncwarp();
+    if (o.n >= 32) {
+        out_flush(a, o, 32, lane);
+        const unsigned rem = o.n - 32;
+        const unsigned long long v = lane < rem ? o.buf[32 + lane] : 0ull;
+        __syncwarp();
+        if (lane < rem)
+            o.buf[lane] = v;
+        __syncwarp();
+        o.n = rem;
+    }
+}
+
+__device__ __forceinline__ void out_finish(const SweepArgs& a, WarpOut& o, unsigned lane)
+{
+    if (o.n)
+        out_flush(a, o, o.n, lane);
+    o.n = 0;
 }
 
 __device__ __forceinline__ bool bf_ok(const SweepArgs& a, unsigned long long p, unsigned long long j)
@@ -545,28 +581,30 @@ constexpr int kUnroll = CCDK_SWEEP_UNROLL;
 constexpr int kHitBuf = 32 * kUnroll + 32; // < 32 left over + kUnroll strides
 
 __device__ __forceinline__ void filter_hits(const SweepArgs& a, unsigned long long p, float4 mb, uint4 mv,
-                                            const unsigned* hits, unsigned cnt, unsigned lane)
+                                            const unsigned* hits, unsigned cnt, unsigned lane, WarpOut& o)
 {
     bool h = lane < cnt;
     const unsigned long long q = p + (h ? hits[lane] : 0u);
-    // the quantised pass is a superset: the exact fp32 test decides
-    h = h && box_hit(mb, a.sbox[q]);
+    // the quantised pass is a superset: the exact fp32 test decides; the box
+    // and the vertex ids load together (one round trip)
+    const float4 ob = a.sbox[q];
+    const uint4 ov = a.svid[q];
+    h = h && box_hit(mb, ob);
     if (a.slab) // slab mode: only the canonical slab of the pair emits it
         h = h && max(a.slab_first[p], a.slab_first[q]) == a.slab[p];
-    const uint4 ov = h ? a.svid[q] : make_uint4(0, 0, 0, 0);
-    emit(a, h && keep_pair(mv, ov) && bf_ok(a, p, q), mv.w, ov.w);
+    out_push(a, o, h && keep_pair(mv, ov) && bf_ok(a, p, q), mv.w, ov.w, lane);
 }
 
 // Run the filter on every full chunk of 32 (all of them when `all`) and
 // move the remainder to the front of the list.
 __device__ __forceinline__ void drain_hits(const SweepArgs& a, unsigned long long p, float4 mb, uint4 mv,
-                                           unsigned* hits, unsigned& nh, unsigned lane, bool all)
+                                           unsigned* hits, unsigned& nh, unsigned lane, bool all, WarpOut& o)
 {
     __syncwarp();
     unsigned base = 0;
     while (nh - base >= 32 || (all && nh > base)) {
         const unsigned cnt = min(nh - base, 32u);
-        filter_hits(a, p, mb, mv, hits + base, cnt, lane);
+        filter_hits(a, p, mb, mv, hits + base, cnt, lane, o);
         base += cnt;
     }
     const unsigned rem = nh - base; // < 32
@@ -600,7 +638,7 @@ __device__ __forceinline__ bool qhit(unsigned m_hi_g, unsigned m_lo, uint2 o)
 
 // Row p against boxes [jb, je) of its window (warp-cooperative).
 __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long long p, unsigned long long jb,
-                                             unsigned long long je, unsigned* hits, unsigned lane)
+                                             unsigned long long je, unsigned* hits, unsigned lane, WarpOut& o)
 {
     const float4 mb = a.sbox[p];
     const uint4 mv = a.svid[p];
@@ -613,14 +651,14 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
     const uint2* qp = a.sq + j0 + lane;
     unsigned off = static_cast<unsigned>(j0 - p) + lane; // this lane's box offset from p
     for (; j0 + 32 * kUnroll <= je; j0 += 32 * kUnroll, qp += 32 * kUnroll, off += 32 * kUnroll) {
-        uint2 o[kUnroll];
+        uint2 qv[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-            o[u] = __ldg(qp + 32 * u);
+            qv[u] = __ldg(qp + 32 * u);
         bool h[kUnroll], any = false;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            h[u] = qhit(m_hi_g, m_lo, o[u]);
+            h[u] = qhit(m_hi_g, m_lo, qv[u]);
             any = any || h[u];
         }
         if (__any_sync(0xffffffffu, any)) {
@@ -628,7 +666,7 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
             for (int u = 0; u < kUnroll; ++u)
                 push_hit(hits, nh, h[u], off + 32 * u, lane);
             if (nh >= 32)
-                drain_hits(a, p, mb, mv, hits, nh, lane, false);
+                drain_hits(a, p, mb, mv, hits, nh, lane, false, o);
         }
     }
     // ragged tail (< 32 kUnroll boxes): lanes past the window end are idle
@@ -639,7 +677,7 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
         push_hit(hits, nh, h, static_cast<unsigned>(j - p), lane);
     }
     if (nh)
-        drain_hits(a, p, mb, mv, hits, nh, lane, true);
+        drain_hits(a, p, mb, mv, hits, nh, lane, true, o);
 }
 
 #ifndef CCDK_SWEEP_MINB
@@ -648,8 +686,10 @@ __device__ __forceinline__ void sweep_window(const SweepArgs& a, unsigned long l
 __global__ void __launch_bounds__(kRowsTB, CCDK_SWEEP_MINB) k_sweep_rows(SweepArgs a)
 {
     __shared__ unsigned s_hits[kRowsTB / 32][kHitBuf];
+    __shared__ unsigned long long s_out[kRowsTB / 32][kOutBuf];
     const unsigned lane = threadIdx.x & 31;
     unsigned* hits = s_hits[threadIdx.x >> 5];
+    WarpOut o { s_out[threadIdx.x >> 5], 0u };
     const unsigned long long B = a.range[0], E = a.range[1];
     const unsigned long long warp = (blockIdx.x * static_cast<unsigned long long>(kRowsTB) + threadIdx.x) >> 5;
     const unsigned long long p0 = a.row0 + warp * kRowsPerWarp;
@@ -659,10 +699,87 @@ __global__ void __launch_bounds__(kRowsTB, CCDK_SWEEP_MINB) k_sweep_rows(SweepAr
             break; // warp-uniform
         if (p < B)
             continue;
-        const unsigned long long je = min(static_cast<unsigned long long>(a.run_end[p]), p + 1 + kCap);
-        if (je > p + 1)
-            sweep_window(a, p, p + 1, je, hits, lane);
+        const unsigned long long re = a.run_end[p];
+        if (re <= p + 1 + a.short_len)
+            continue; // empty, or a short window (k_sweep_short)
+        const unsigned long long je = min(re, p + 1 + a.row_cap);
+        sweep_window(a, p, p + 1, je, hits, lane, o);
     }
+    out_finish(a, o, lane);
+}
+
+// Short windows (slab mode: ~20 boxes per window, so a warp per row would
+// leave most lanes idle and pay the per-row set-up 1.5M times): one LANE per
+// row, the warp stepping through its 32 rows' windows in lockstep (trip count
+// = the longest of them, <= short_len).  Quantised hits are compacted as
+// (owner lane, other entry) into a per-warp list and the exact test,
+// keep_pair and the slab dedup run on 32 of them at a time with every lane
+// busy, emitted with one warp-aggregated atomic.
+constexpr int kShortBuf = 64;
+
+__device__ __forceinline__ void short_filter(const SweepArgs& a, unsigned long long p_base, const uint2* hits,
+                                             unsigned cnt, unsigned lane, WarpOut& o)
+{
+    bool h = lane < cnt;
+    const uint2 e = h ? hits[lane] : make_uint2(0, 0);
+    const unsigned long long p = p_base + e.x, q = e.y;
+    // every operand in one round trip (no load waits on another's test)
+    const float4 mb = a.sbox[p], ob = a.sbox[q];
+    const uint4 mv = a.svid[p], ov = a.svid[q];
+    h = h && box_hit(mb, ob);
+    if (a.slab)
+        h = h && max(a.slab_first[p], a.slab_first[q]) == a.slab[p];
+    out_push(a, o, h && keep_pair(mv, ov), mv.w, ov.w, lane);
+}
+
+__global__ void __launch_bounds__(kRowsTB) k_sweep_short(SweepArgs a)
+{
+    __shared__ uint2 s_hits[kRowsTB / 32][kShortBuf];
+    __shared__ unsigned long long s_out[kRowsTB / 32][kOutBuf];
+    const unsigned lane = threadIdx.x & 31;
+    uint2* hits = s_hits[threadIdx.x >> 5];
+    WarpOut o { s_out[threadIdx.x >> 5], 0u };
+    const unsigned long long B = a.range[0], E = a.range[1];
+    const unsigned long long p_base = a.row0 + ((blockIdx.x * static_cast<unsigned long long>(kRowsTB) + threadIdx.x) & ~31ull);
+    if (p_base >= E)
+        return; // warp-uniform
+    const unsigned long long p = p_base + lane;
+    unsigned len = 0;
+    uint2 mq = make_uint2(0, 0);
+    if (p >= B && p < E) {
+        const unsigned long long re = a.run_end[p];
+        if (re > p + 1 && re <= p + 1 + a.short_len) {
+            len = static_cast<unsigned>(re - p - 1);
+            mq = a.sq[p];
+        }
+    }
+    const unsigned maxlen = __reduce_max_sync(0xffffffffu, len);
+    const unsigned lt = (1u << lane) - 1;
+    unsigned nh = 0; // warp-uniform
+    for (unsigned t = 0; t < maxlen; ++t) {
+        const unsigned long long q = p + 1 + t;
+        const bool h = t < len && qhit(mq.y, mq.x, __ldg(&a.sq[q]));
+        const unsigned m = __ballot_sync(0xffffffffu, h);
+        if (h)
+            hits[nh + __popc(m & lt)] = make_uint2(lane, static_cast<unsigned>(q));
+        nh += __popc(m);
+        if (nh >= 32) {
+            __syncwarp();
+            short_filter(a, p_base, hits, 32, lane, o);
+            const unsigned rem = nh - 32;
+            const uint2 v = lane < rem ? hits[32 + lane] : make_uint2(0, 0);
+            __syncwarp();
+            if (lane < rem)
+                hits[lane] = v;
+            __syncwarp();
+            nh = rem;
+        }
+    }
+    if (nh) {
+        __syncwarp();
+        short_filter(a, p_base, hits, nh, lane, o);
+    }
+    out_finish(a, o, lane);
 }
 
 // Heavy rows: one warp per (row, kSeg-long window segment) — the part of a
@@ -670,15 +787,18 @@ __global__ void __launch_bounds__(kRowsTB, CCDK_SWEEP_MINB) k_sweep_rows(SweepAr
 __global__ void __launch_bounds__(kRowsTB) k_sweep_heavy(SweepArgs a)
 {
     __shared__ unsigned s_hits[kRowsTB / 32][kHitBuf];
+    __shared__ unsigned long long s_out[kRowsTB / 32][kOutBuf];
     const unsigned lane = threadIdx.x & 31;
     unsigned* hits = s_hits[threadIdx.x >> 5];
+    WarpOut o { s_out[threadIdx.x >> 5], 0u };
     const unsigned long long nseg = *a.n_heavy;
     const unsigned long long warp = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5;
     const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
     for (unsigned long long sg = warp; sg < nseg; sg += nwarps) {
         const Seg g = a.segs[sg];
-        sweep_window(a, g.p, g.jb, g.je, hits, lane);
+        sweep_window(a, g.p, g.jb, g.je, hits, lane, o);
     }
+    out_finish(a, o, lane);
 }
 
 // ---- K5' slab mode.  The candidate set is a property of the boxes alone
@@ -704,6 +824,9 @@ struct SlabParams {
     int ok;
 };
 constexpr unsigned kMaxSlabs = 65535; // slab ids sort on 16 bits
+constexpr unsigned kShortLen = 64;    // slab-mode windows up to this run one lane per row
+constexpr uint32_t kSlabCap = 256;    // slab mode: row cap and heavy segment length
+constexpr uint64_t kSlabMinBoxes = 200000; // measured crossover (C1 75k: 1-D faster; C2 300k: slab faster)
 
 __device__ __forceinline__ unsigned slab_of(const SlabParams& P, float x)
 {
@@ -958,8 +1081,12 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     const uint32_t* w_first = nullptr;
     unsigned long long* d_range = &ctr->misc[0]; // misc[0..1]
     uint32_t* run_end = nullptr;
-    static const bool slab_env_off = std::getenv("CCDK_SLAB") && std::getenv("CCDK_SLAB")[0] == '0';
-    const bool slab_try = !bf && !slab_env_off && lo == 0 && hi == k - 1 && in.shard_count == 1
+    // CCDK_SLAB=0 / =1 forces the 1-D / slab sweep; by default slab mode from
+    // kSlabMinBoxes on (below it the set-up's ~10 launches and host read-back
+    // cost more than the shorter windows save: C1, 75k boxes, 0.17 -> 0.24 ms)
+    const char* slab_env = std::getenv("CCDK_SLAB"); // read per call: tests toggle it
+    const bool slab_size_ok = slab_env ? slab_env[0] != '0' : k >= kSlabMinBoxes;
+    const bool slab_try = !bf && slab_size_ok && lo == 0 && hi == k - 1 && in.shard_count == 1
         && !in.want_rounds && k < (uint64_t(1) << 30);
     if (slab_try) {
         char* par = static_cast<char*>(c.slab_par.ensure(64));
@@ -1041,13 +1168,16 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         }
         CCDK_LAUNCH_CHECK();
     }
+    // slab mode: long rows (boxes spanning a slab, e.g. a static floor) split
+    // into short segments so no single warp walks thousands of hits
+    const uint32_t cap = out.slab_mode ? kSlabCap : kCap, seg = out.slab_mode ? kSlabCap : kSeg;
     uint32_t* nseg = grow<uint32_t>(c.seg_off, 2 * rows);
     uint32_t* off = nseg + rows;
-    k_heavy_count<<<grid_for(rows, 256), 256, 0, s>>>(run_end, d_range, rows, nseg);
+    k_heavy_count<<<grid_for(rows, 256), 256, 0, s>>>(run_end, d_range, rows, nseg, cap, seg);
     cub_call(c, [&](void* t, size_t& b) {
         return cub::DeviceScan::ExclusiveSum(t, b, nseg, off, static_cast<int64_t>(rows), s);
     });
-    // segments total <= sum over rows of ceil(k / kSeg); grow on demand below
+    // segments total <= sum over rows of ceil(window / seg); grow on demand below
     uint64_t seg_cap = std::max<uint64_t>(c.segs.cap / sizeof(Seg), 1024);
     Seg* segs = grow<Seg>(c.segs, seg_cap);
 
@@ -1097,7 +1227,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
             CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
         }
     }
-    k_heavy_gen<<<grid_for(rows, 256), 256, 0, s>>>(run_end, nseg, off, rows, segs, &ctr->n_heavy);
+    k_heavy_gen<<<grid_for(rows, 256), 256, 0, s>>>(run_end, nseg, off, rows, segs, &ctr->n_heavy, cap, seg);
     CCDK_LAUNCH_CHECK();
 
     // K5 sweep (re-run once with a larger buffer if the candidate count overflows)
@@ -1131,9 +1261,13 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         sa.n_pairs = &ctr->n_pairs;
         sa.segs = segs;
         sa.n_heavy = &ctr->n_heavy;
+        sa.short_len = out.slab_mode ? kShortLen : 0;
+        sa.row_cap = cap;
         if (hi > lo) {
             const uint64_t warps = (hi - lo + kRowsPerWarp - 1) / kRowsPerWarp;
             k_sweep_rows<<<grid_for(warps * 32, kRowsTB), kRowsTB, 0, s>>>(sa);
+            if (sa.short_len)
+                k_sweep_short<<<grid_for(hi - lo, kRowsTB), kRowsTB, 0, s>>>(sa);
         }
         k_sweep_heavy<<<4 * c.num_sms, kRowsTB, 0, s>>>(sa);
         CCDK_LAUNCH_CHECK();
