@@ -857,7 +857,7 @@ __global__ void k_slab_stats(const float4* sbox, unsigned long long k, double* s
 // slab axis = the wider of the two non-sweep axes; width = 2 x its mean box
 // extent (at least ext / kMaxSlabs); ok = finite bounds and >= 2 slabs
 __global__ void k_slab_params(const unsigned* qb, const int* axis, const double* sums, unsigned long long k,
-                              SlabParams* P)
+                              double width_factor, SlabParams* P)
 {
     const int a = *axis, a1 = (a + 1) % 3, a2 = (a + 2) % 3;
     const float lo1 = ord2f(qb[a1]), hi1 = ord2f(qb[3 + a1]);
@@ -869,7 +869,7 @@ __global__ void k_slab_params(const unsigned* qb, const int* axis, const double*
     const double mean = sums[side] / static_cast<double>(k);
     SlabParams p { lo, 0.0f, 1u, side, 0 };
     if (isfinite(lo1) && isfinite(hi1) && isfinite(lo2) && isfinite(hi2) && ext > 0.0) {
-        const double w = fmax(2.0 * mean, ext / kMaxSlabs);
+        const double w = fmax(width_factor * mean, ext / kMaxSlabs);
         const double S = ceil(ext / w);
         if (S >= 2.0 && w > 0.0) {
             p.S = static_cast<unsigned>(fmin(S, static_cast<double>(kMaxSlabs)));
@@ -1094,7 +1094,8 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         SlabParams* P = reinterpret_cast<SlabParams*>(par + 16);
         CCDK_CUDA_CHECK(cudaMemsetAsync(sums, 0, 16, s));
         k_slab_stats<<<kRedBlocks, kRedThreads, 0, s>>>(sbox, k, sums);
-        k_slab_params<<<1, 1, 0, s>>>(qb, d_axis, sums, k, P);
+        const char* wf = std::getenv("CCDK_SLAB_W"); // slab width / mean box extent (tuning)
+        k_slab_params<<<1, 1, 0, s>>>(qb, d_axis, sums, k, wf ? std::atof(wf) : 2.0, P);
         uint32_t* cnt = grow<uint32_t>(c.slab_cnt, 2 * k);
         uint32_t* eoff = cnt + k;
         k_slab_count<<<grid_for(k, 256), 256, 0, s>>>(sbox, k, P, cnt);
