@@ -556,7 +556,8 @@ struct BatchRun {
 
     // broad_batch (pipeline.cpp:140-174): halve the sweep range while the
     // candidates exceed the budget's pair capacity
-    void broad_batch(uint64_t begin, uint64_t end, uint32_t shard_rank = 0, uint32_t shard_count = 1)
+    void broad_batch(uint64_t begin, uint64_t end, uint32_t shard_rank = 0, uint32_t shard_count = 1,
+                     bool allow_slab = true)
     {
         BroadIn bi;
         bi.bmin = bmin;
@@ -570,6 +571,7 @@ struct BatchRun {
         bi.shard_count = shard_count;
         // the axis matters only if the budget can force range halving
         bi.exact_axis = cap_pairs < k * (k - 1) / 2;
+        bi.allow_slab = allow_slab;
         BroadOut bo;
         broad_phase(c, bi, bo);
         launches += bi.exact_axis ? 12 : 11;
@@ -580,6 +582,11 @@ struct BatchRun {
         axis = bo.axis;
         slabs = bo.slab_count;
         slab_entries = bo.slab_entries;
+        if (shard_count > 1 && bo.slab_mode && bo.n_pairs > cap_pairs) {
+            // budget halving is defined on sorted positions: redo this shard 1-D
+            broad_batch(begin, end, shard_rank, shard_count, false);
+            return;
+        }
         if (shard_count > 1) { // this shard's slice of sorted left positions
             begin = bo.range_lo;
             end = bo.range_hi;

@@ -932,6 +932,13 @@ __global__ void k_slab_gather(const uint32_t* keys, const uint32_t* vals, unsign
         slab_end[s] = static_cast<uint32_t>(e + 1);
 }
 
+__global__ void k_entry_len(const uint32_t* run_end, unsigned long long E, unsigned long long* len)
+{
+    const unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (e < E)
+        len[e] = run_end[e] - e - 1;
+}
+
 // K4 per entry: the window ends at the first entry of the same slab whose
 // min-a exceeds this entry's max-a
 __global__ void k_slab_run_ends(const float* emin_a, const float* emax_a, const uint32_t* eslab,
@@ -1086,8 +1093,8 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     // cost more than the shorter windows save: C1, 75k boxes, 0.17 -> 0.24 ms)
     const char* slab_env = std::getenv("CCDK_SLAB"); // read per call: tests toggle it
     const bool slab_size_ok = slab_env ? slab_env[0] != '0' : k >= kSlabMinBoxes;
-    const bool slab_try = !bf && slab_size_ok && lo == 0 && hi == k - 1 && in.shard_count == 1
-        && !in.want_rounds && k < (uint64_t(1) << 30);
+    const bool slab_try = !bf && in.allow_slab && slab_size_ok && lo == 0 && hi == k - 1 && !in.want_rounds
+        && k < (uint64_t(1) << 30);
     if (slab_try) {
         char* par = static_cast<char*>(c.slab_par.ensure(64));
         double* sums = reinterpret_cast<double*>(par);
@@ -1133,7 +1140,19 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
             run_end = grow<uint32_t>(c.run_end, E);
             k_slab_run_ends<<<grid_for(E, 256), 256, 0, s>>>(emin, emax, eslab, slab_end, E, run_end,
                                                               &ctr->pair_tests);
-            k_full_range<<<1, 1, 0, s>>>(0, E, d_range);
+            if (in.shard_count > 1) {
+                // multi-GPU: rank r sweeps the entry rows [B_r, B_{r+1}) that split
+                // the total window length evenly (every pair has exactly one
+                // emitting row, so any partition of rows partitions the pairs)
+                unsigned long long* len = grow<unsigned long long>(c.prefix, 2 * E);
+                k_entry_len<<<grid_for(E, 256), 256, 0, s>>>(run_end, E, len);
+                cub_call(c, [&](void* t, size_t& b) {
+                    return cub::DeviceScan::InclusiveSum(t, b, len, len + E, static_cast<int64_t>(E), s);
+                });
+                k_shard_range<<<1, 32, 0, s>>>(len + E, 0, E, in.shard_rank, in.shard_count, d_range);
+            } else {
+                k_full_range<<<1, 1, 0, s>>>(0, E, d_range);
+            }
             CCDK_LAUNCH_CHECK();
             rows = E;
             lo = 0;

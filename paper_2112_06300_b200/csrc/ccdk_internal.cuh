@@ -275,6 +275,7 @@ struct BroadIn {
     // reproduce choose_axis's serial summation order on near ties (the axis
     // is observable through choose_axis, StqStats and SweepRange slices)
     bool exact_axis = true;
+    bool allow_slab = true; // slab-mode sweep permitted (full range, no StqStats)
 };
 void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out);
 

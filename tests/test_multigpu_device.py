@@ -32,9 +32,12 @@ def _free_port():
 SCENE = dict(nx=40, ny=40, jitter=0.02, drop=1.0, seed=4)
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, slab="auto"):
     import torch
     import torch.distributed as dist
+
+    if slab != "auto":
+        os.environ["CCDK_SLAB"] = slab  # force the slab-mode sweep (shards over entry rows)
 
     from paper_2112_06300_b200 import ccdkit as ck, native, scenes
     from paper_2112_06300_b200.multigpu import RebalancedCcd, ShardedCcd
@@ -75,13 +78,14 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_world2_on_one_device_matches_single_process(tmp_path):
+@pytest.mark.parametrize("slab", ["auto", "1"])
+def test_world2_on_one_device_matches_single_process(tmp_path, slab):
     import torch.multiprocessing as mp
 
     import oracle
     from paper_2112_06300_b200 import abi, scenes
 
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), slab), nprocs=2, join=True)
     res = np.load(tmp_path / "res.npz")
     s = scenes.make_cloth_scene(SCENE["nx"], SCENE["ny"], SCENE["jitter"], SCENE["drop"], SCENE["seed"])
     rep, pairs = oracle.orc().ccd(s, abi.pipeline_cfg(inflation=0.01))

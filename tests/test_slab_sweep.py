@@ -89,3 +89,34 @@ def test_slab_mode_runs_on_a_full_step(ctx, ref):
         rep1 = ck.ccd(s, cfg, ctx=ctx)
     assert rep1.device["sweep_slabs"] == 0
     np.testing.assert_array_equal(rep1.candidates, pairs)
+
+
+@pytest.mark.parametrize("shards", [2, 3, 8])
+def test_slab_mode_shards_partition_the_set(ctx, ref, shards):
+    """Multi-GPU broad phase in slab mode: rank r sweeps the entry rows that
+    split the total window length evenly; the shards' keys are disjoint and
+    union to the full candidate set."""
+    import torch
+    s = scenes.make_box_soup(2500, 22.0, 0.35, 1.2, 17)
+    cfg = ck.PipelineConfig(inflation=0.01)
+    rs = ck.ResidentScene(s, ctx)
+    with _Slab("1"):
+        n_all, nb, _ = rs.broad(cfg, 0, 1)
+        t = torch.empty(max(n_all, 1), dtype=torch.int64, device="cuda")
+        rs.copy_keys(t.data_ptr())
+        full = np.sort(t[:n_all].cpu().numpy().view(np.uint64))
+        parts = []
+        for r in range(shards):
+            n, nb2, _ = rs.broad(cfg, r, shards)
+            assert nb2 == nb
+            t = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+            rs.copy_keys(t.data_ptr())
+            parts.append(t[:n].cpu().numpy().view(np.uint64))
+        rep = rs.step(cfg)
+        assert rep.device["sweep_slabs"] > 1
+    concat = np.concatenate(parts)
+    assert len(np.unique(concat)) == len(concat)  # disjoint
+    np.testing.assert_array_equal(np.sort(concat), full)
+    b = ck.build_boxes(s, 0.01, ctx=ctx)
+    exp, _, _ = ref.broad(abi.BROAD_STQ, b.as_tuple(), s)
+    assert len(full) == len(exp)
