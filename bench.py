@@ -534,14 +534,16 @@ def run_ours(args):
     roofline = {"kernel": "k_generation (BFS narrow phase, all generations of one step)",
                 "bound": "fp64", "achieved": narrow_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": narrow_tf / fp64_peak, "traffic": traffic.get("k_generation_bytes_per_launch"),
-                "traffic_note": traffic.get("note"),
+                "traffic_note": traffic.get("k_generation_note", traffic.get("note")),
                 "peak_source": "measured DADD rate 62.7/SM/clk (profiles/r01_ubench_fp64.txt) x 148 SMs x "
                                "sampled SM clock; bound is the fp64 pipe (neither HBM nor tensor cores: "
                                "bit-exact fp64 interval arithmetic, no FMA)",
                 "algorithmic": f"F = 339*E + 96*S, E={d['evaluations']}, S={d['split_actions']}"}
-    roofline_sweep = {"kernel": "run ends + tile sweep + heavy sweep", "bound": "hbm",
+    roofline_sweep = {"kernel": "K4+K5 sweep stage (slab set-up or run ends, heavy segments, row / short / heavy "
+                                "sweep kernels)", "bound": "hbm",
                       "achieved": sweep_gbs, "peak": hbm_peak, "unit": "GB/s",
-                      "frac": sweep_gbs / hbm_peak, "traffic": traffic.get("k_sweep_rows_bytes_per_launch"),
+                      "frac": sweep_gbs / hbm_peak,
+                      "traffic": traffic.get("sweep_bytes_per_step", traffic.get("k_sweep_rows_bytes_per_launch")),
                       "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                       "algorithmic": f"B = 40k + 8C, k={k}, C={rep.candidate_count}",
                       "pair_tests": d["pair_tests"],

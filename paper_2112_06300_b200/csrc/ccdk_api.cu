@@ -574,7 +574,7 @@ struct BatchRun {
         bi.allow_slab = allow_slab;
         BroadOut bo;
         broad_phase(c, bi, bo);
-        launches += bi.exact_axis ? 12 : 11;
+        launches += bo.launches;
         pair_tests += bo.pair_tests;
         ms_sort += bo.ms_axis_sort;
         ms_sweep += bo.ms_sweep;

@@ -1032,15 +1032,20 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     int* d_axis = static_cast<int*>(c.axis.ensure(64));
     double* part = grow<double>(c.partials, 9 * kRedBlocks);
     CCDK_CUDA_CHECK(cudaMemsetAsync(d_axis, 0, 4 * sizeof(int), s));
+    ++out.launches;
     k_axis_sum<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, part);
+    ++out.launches;
     k_axis_var<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, part, part + 3 * kRedBlocks);
+    ++out.launches;
     k_axis_pick<<<1, kRedThreads, 0, s>>>(part, k, d_axis);
     // The candidate set does not depend on the axis; the axis is observable
     // only through choose_axis itself, StqStats and SweepRange slices (and the
     // budget batching built on them), so the exact serial order is enforced
     // where those are requested.
-    if (in.exact_axis)
+    if (in.exact_axis) {
+        ++out.launches;
         k_axis_serial<<<1, 96, 0, s>>>(in.bmin, in.bmax, k, d_axis);
+    }
     CCDK_LAUNCH_CHECK();
 
     // K3 sort + permute
@@ -1048,6 +1053,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     uint32_t* keys_out = grow<uint32_t>(c.sort_keys_out, k);
     uint32_t* vals_in = grow<uint32_t>(c.sort_vals_in, k);
     uint32_t* order = grow<uint32_t>(c.sort_vals_out, k);
+    ++out.launches;
     k_sort_keys<<<grid_for(k, 256), 256, 0, s>>>(in.bmin, k, d_axis, keys_in, vals_in);
     CCDK_LAUNCH_CHECK();
     cub_call(c, [&](void* t, size_t& b) {
@@ -1063,8 +1069,10 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     unsigned* qb = static_cast<unsigned*>(c.qbounds.ensure(8 * sizeof(unsigned)));
     CCDK_CUDA_CHECK(cudaMemsetAsync(qb, 0xff, 3 * sizeof(unsigned), s));
     CCDK_CUDA_CHECK(cudaMemsetAsync(qb + 3, 0, 3 * sizeof(unsigned), s));
+    ++out.launches;
     k_quant_bounds<<<kRedBlocks, kRedThreads, 0, s>>>(in.bmin, in.bmax, k, qb);
     uint2* sq = grow<uint2>(c.squant, k);
+    ++out.launches;
     k_permute<<<grid_for(k, 256), 256, 0, s>>>(in.bmin, in.bmax, in.vids, in.raw, k, d_axis, order,
                                                smin_a, smax_a, sbox, svid, sraw, qb, sq);
     CCDK_LAUNCH_CHECK();
@@ -1100,11 +1108,14 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         double* sums = reinterpret_cast<double*>(par);
         SlabParams* P = reinterpret_cast<SlabParams*>(par + 16);
         CCDK_CUDA_CHECK(cudaMemsetAsync(sums, 0, 16, s));
+        ++out.launches;
         k_slab_stats<<<kRedBlocks, kRedThreads, 0, s>>>(sbox, k, sums);
         const char* wf = std::getenv("CCDK_SLAB_W"); // slab width / mean box extent (tuning)
+        ++out.launches;
         k_slab_params<<<1, 1, 0, s>>>(qb, d_axis, sums, k, wf ? std::atof(wf) : 2.0, P);
         uint32_t* cnt = grow<uint32_t>(c.slab_cnt, 2 * k);
         uint32_t* eoff = cnt + k;
+        ++out.launches;
         k_slab_count<<<grid_for(k, 256), 256, 0, s>>>(sbox, k, P, cnt);
         CCDK_LAUNCH_CHECK();
         cub_call(c, [&](void* t, size_t& b) {
@@ -1121,6 +1132,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         if (hp.ok && E <= 4 * k) {
             uint32_t* ek = grow<uint32_t>(c.slab_keys, 2 * E);
             uint32_t* ev_ = grow<uint32_t>(c.slab_vals, 2 * E);
+            ++out.launches;
             k_slab_emit<<<grid_for(k, 256), 256, 0, s>>>(sbox, k, P, eoff, ek, ev_);
             CCDK_LAUNCH_CHECK();
             cub_call(c, [&](void* t, size_t& b) { // stable: each slab stays in min-a order
@@ -1135,9 +1147,11 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
             uint32_t* eslab = grow<uint32_t>(c.eslab, 2 * E);
             uint32_t* efirst = eslab + E;
             uint32_t* slab_end = grow<uint32_t>(c.slab_end, hp.S);
+            ++out.launches;
             k_slab_gather<<<grid_for(E, 256), 256, 0, s>>>(ek + E, ev_ + E, E, P, smin_a, smax_a, sbox, svid, sq,
                                                             emin, emax, ebox, evid, eq, eslab, efirst, slab_end);
             run_end = grow<uint32_t>(c.run_end, E);
+            ++out.launches;
             k_slab_run_ends<<<grid_for(E, 256), 256, 0, s>>>(emin, emax, eslab, slab_end, E, run_end,
                                                               &ctr->pair_tests);
             if (in.shard_count > 1) {
@@ -1145,12 +1159,15 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
                 // the total window length evenly (every pair has exactly one
                 // emitting row, so any partition of rows partitions the pairs)
                 unsigned long long* len = grow<unsigned long long>(c.prefix, 2 * E);
+                ++out.launches;
                 k_entry_len<<<grid_for(E, 256), 256, 0, s>>>(run_end, E, len);
                 cub_call(c, [&](void* t, size_t& b) {
                     return cub::DeviceScan::InclusiveSum(t, b, len, len + E, static_cast<int64_t>(E), s);
                 });
+                ++out.launches;
                 k_shard_range<<<1, 32, 0, s>>>(len + E, 0, E, in.shard_rank, in.shard_count, d_range);
             } else {
+                ++out.launches;
                 k_full_range<<<1, 1, 0, s>>>(0, E, d_range);
             }
             CCDK_LAUNCH_CHECK();
@@ -1174,6 +1191,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     if (!out.slab_mode) {
         run_end = grow<uint32_t>(c.run_end, k);
         run_len = need_len ? grow<unsigned long long>(c.prefix, 2 * k) : nullptr;
+        ++out.launches;
         k_run_ends<<<grid_for(k, 256), 256, 0, s>>>(smin_a, smax_a, k, lo, hi, run_end, run_len,
                                                      &ctr->pair_tests);
         CCDK_LAUNCH_CHECK();
@@ -1182,8 +1200,10 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
             cub_call(c, [&](void* t, size_t& b) {
                 return cub::DeviceScan::InclusiveSum(t, b, run_len, incl, static_cast<int64_t>(k), s);
             });
+            ++out.launches;
             k_shard_range<<<1, 32, 0, s>>>(incl, lo, hi, in.shard_rank, in.shard_count, d_range);
         } else {
+            ++out.launches;
             k_full_range<<<1, 1, 0, s>>>(lo, hi, d_range);
         }
         CCDK_LAUNCH_CHECK();
@@ -1193,6 +1213,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     const uint32_t cap = out.slab_mode ? kSlabCap : kCap, seg = out.slab_mode ? kSlabCap : kSeg;
     uint32_t* nseg = grow<uint32_t>(c.seg_off, 2 * rows);
     uint32_t* off = nseg + rows;
+    ++out.launches;
     k_heavy_count<<<grid_for(rows, 256), 256, 0, s>>>(run_end, d_range, rows, nseg, cap, seg);
     cub_call(c, [&](void* t, size_t& b) {
         return cub::DeviceScan::ExclusiveSum(t, b, nseg, off, static_cast<int64_t>(rows), s);
@@ -1205,6 +1226,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     if (in.want_rounds) {
         unsigned long long* hist = grow<unsigned long long>(c.rounds, 2 * (k + 1));
         CCDK_CUDA_CHECK(cudaMemsetAsync(hist, 0, (k + 1) * sizeof(unsigned long long), s));
+        ++out.launches;
         k_run_hist<<<grid_for(k, 256), 256, 0, s>>>(run_len, k, hist, &ctr->misc[2]);
         CCDK_LAUNCH_CHECK();
     }
@@ -1234,12 +1256,14 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         if (max_run) {
             unsigned long long* hist = c.rounds.as<unsigned long long>();
             unsigned long long* rev = hist + (k + 1);
+            ++out.launches;
             k_reverse<<<grid_for(max_run, 256), 256, 0, s>>>(hist, max_run, max_run, rev);
             unsigned long long* scan = hist; // reuse: hist no longer needed after reversing
             cub_call(c, [&](void* t, size_t& b) {
                 return cub::DeviceScan::InclusiveSum(t, b, rev, scan, static_cast<int64_t>(max_run), s);
             });
             // scan[i] = sum_{x >= max_run - i} hist[x] = round_sizes[max_run - 1 - i]
+            ++out.launches;
             k_reverse<<<grid_for(max_run, 256), 256, 0, s>>>(scan, max_run, max_run - 1, rev);
             CCDK_LAUNCH_CHECK();
             CCDK_CUDA_CHECK(cudaMemcpyAsync(c.last_rounds.data(), rev, max_run * 8,
@@ -1247,6 +1271,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
             CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
         }
     }
+    ++out.launches;
     k_heavy_gen<<<grid_for(rows, 256), 256, 0, s>>>(run_end, nseg, off, rows, segs, &ctr->n_heavy, cap, seg);
     CCDK_LAUNCH_CHECK();
 
@@ -1285,10 +1310,14 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         sa.row_cap = cap;
         if (hi > lo) {
             const uint64_t warps = (hi - lo + kRowsPerWarp - 1) / kRowsPerWarp;
+            ++out.launches;
             k_sweep_rows<<<grid_for(warps * 32, kRowsTB), kRowsTB, 0, s>>>(sa);
-            if (sa.short_len)
+            if (sa.short_len) {
+                ++out.launches;
                 k_sweep_short<<<grid_for(hi - lo, kRowsTB), kRowsTB, 0, s>>>(sa);
+            }
         }
+        ++out.launches;
         k_sweep_heavy<<<4 * c.num_sms, kRowsTB, 0, s>>>(sa);
         CCDK_LAUNCH_CHECK();
         read_ctr();

@@ -257,6 +257,7 @@ struct BroadOut {
     bool axis_serial = false;   // ... and the reference's serial order decided the axis
     float ms_axis_sort = 0, ms_sweep = 0, ms_pairsort = 0;
     bool slab_mode = false;     // the sweep ran per slab (K5'); entries = boxes incl. slab copies
+    uint64_t launches = 0;      // own (non-CUB) kernels launched
     uint64_t slab_count = 0, slab_entries = 0;
 };
 // General broad phase over SoA boxes whose slot order is owner order (rank =

@@ -12,12 +12,24 @@ import json
 import os
 import sys
 
-STAGES = {
-    "build": lambda n: n == "k_build_boxes",
-    "sort": lambda n: n in ("k_axis_sum", "k_axis_var", "k_axis_pick", "k_sort_keys", "k_permute",
-                            "k_quant_bounds") or ("cub::" in n and "unsigned int" in n and "Radix" in n),
-    "pairsort": lambda n: "cub::" in n and "unsigned long long" in n and "Radix" in n,
-}
+# stage of each launch, by the step's launch order: K1 | K2+K3 (axis, key
+# build, radix sort, permute + quantise) | K4+K5 (slab set-up or run ends,
+# heavy segments, sweep) | K6 pair sort | the rest (classify, narrow)
+def stage_of(seq):
+    stage, out = "other", []
+    for n in seq:
+        if n == "k_build_boxes":
+            stage = "build"
+        elif n == "k_axis_sum":
+            stage = "sort"
+        elif n in ("k_slab_stats", "k_run_ends"):
+            stage = "sweep"
+        elif stage == "sweep" and "policy_hub<unsigned long long" in n and "Radix" in n:
+            stage = "pairsort"
+        elif n in ("k_classify_keys", "k_init_scalars"):
+            stage = "other"
+        out.append(stage)
+    return out
 
 
 def main(path, out_txt):
@@ -31,6 +43,8 @@ def main(path, out_txt):
         d[r[mi]] = float(r[vi].replace(",", ""))
     ids = sorted(data)
     second = [data[i] for i in ids if i >= ids[len(ids) // 2]]
+    for d, st in zip(second, stage_of([d["name"] for d in second])):
+        d["stage"] = st
     agg = collections.OrderedDict()
     for d in second:
         a = agg.setdefault(d["name"], [0, 0.0, 0.0])
@@ -43,9 +57,9 @@ def main(path, out_txt):
     for name, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"{t:9.1f} {100 * t / tot_t:5.1f}% {n:4d} {b / 1e6:9.2f} {b / 1e3 / t if t else 0:7.0f}  {name[:110]}")
     stage = {}
-    for s, pred in STAGES.items():
-        t = sum(a[1] for n, a in agg.items() if pred(n))
-        b = sum(a[2] for n, a in agg.items() if pred(n))
+    for s in ("build", "sort", "sweep", "pairsort"):
+        t = sum(d["gpu__time_duration.sum"] / 1e3 for d in second if d["stage"] == s)
+        b = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in second if d["stage"] == s)
         stage[s] = (t, b)
         lines.append(f"# stage {s}: {t:.1f} us kernel time, {b / 1e6:.2f} MB DRAM, {b / 1e3 / t if t else 0:.0f} GB/s")
     open(out_txt, "w").write("\n".join(lines) + "\n")
