@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CCDK_ABI_VERSION 1
+#define CCDK_ABI_VERSION 2 /* 2: ccdk_report gained sweep_slabs, sweep_entries; ccdk_ccd_into */
 
 #if defined(__GNUC__)
 #define CCDK_API __attribute__((visibility("default")))

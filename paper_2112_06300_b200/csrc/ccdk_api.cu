@@ -420,7 +420,7 @@ void upload_pieces(Ctx& c, const HostPiece* pieces, int n)
         }
     };
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned helpers = static_cast<unsigned>(std::min<size_t>({ 3, hw / 2, chunks.size() / 2 }));
+    const unsigned helpers = static_cast<unsigned>(std::min<size_t>({ 7, hw / 2, chunks.size() / 2 }));
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < helpers; ++t)
         pool.emplace_back(work);

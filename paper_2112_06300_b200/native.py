@@ -111,7 +111,7 @@ def lib():
                     f = getattr(L, name)
                     f.restype = res
                     f.argtypes = args
-                if L.ccdk_abi_version() != 1:
+                if L.ccdk_abi_version() != 2:
                     raise ImportError("libccdk.so ABI version mismatch")
                 _lib = L
     return _lib

@@ -25,7 +25,7 @@ def test_library_loads_and_exports_all_symbols():
     lib = native.lib()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.ccdk_abi_version() == 1
+    assert lib.ccdk_abi_version() == 2
 
 
 def test_no_device_fails_loudly_without_fallback():
