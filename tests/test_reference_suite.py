@@ -64,6 +64,19 @@ def test_reference_oracle_cases_on_cpu(tmp_path):
     assert "| 0 failed" in r.stdout
 
 
+@pytest.mark.parametrize("name,cases", [
+    ("test_geometry", "scene validation,OBJ,manifest"),
+    ("test_bench", "generated scenes,CSV report,JSON report,loglog_slope"),
+])
+def test_reference_host_cases_on_cpu(tmp_path, name, cases):
+    """The reference's own cases that exercise only host code of the drop-in
+    (SceneStep::validate, OBJ / manifest ingestion, the seeded generators,
+    CSV / JSON reports) pass without a device."""
+    r = _run([_bin(name), "-tc=" + cases], str(tmp_path), timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "| 0 failed" in r.stdout and "test cases: 0 " not in r.stdout
+
+
 def test_ccdbench_usage_errors(tmp_path):
     exe = os.path.join(LIB, "ccdbench")
     if not os.path.exists(exe):
