@@ -593,10 +593,18 @@ CCDKIT_EXPORT ToiResult run_batched(const SceneStep& scene, const std::vector<Aa
                    edata(scene), scene.edges.size(), fdata(scene), scene.faces.size(), &c, &r));
     trace.broad_batches += r.broad_batches;
     trace.narrow_batches += r.batch_count;
-    if (report) {
-        const size_t peak = report->tracked_peak_bytes;
-        *report = to_report(r, true);
-        report->tracked_peak_bytes = std::max(peak, report->tracked_peak_bytes);
+    if (report) { // exactly the fields the reference's run_batched writes (pipeline.cpp:198-214)
+        CcdReport fresh = to_report(r, true);
+        report->toi = fresh.toi;
+        report->candidate_count = fresh.candidate_count;
+        report->query_count = fresh.query_count;
+        report->batch_count = fresh.batch_count;
+        report->per_stage_times["BP"] = fresh.per_stage_times["BP"];
+        report->per_stage_times["SO/CD"] = fresh.per_stage_times["SO/CD"];
+        report->per_stage_times["NP"] = fresh.per_stage_times["NP"];
+        report->tracked_peak_bytes = std::max(report->tracked_peak_bytes, fresh.tracked_peak_bytes);
+        report->candidates = std::move(fresh.candidates);
+        report->real_record_sizes = fresh.real_record_sizes;
     }
     return { r.toi, r.tolerance_hit != 0, r.zero_toi_diagnostic != 0 };
 }
