@@ -621,8 +621,32 @@ struct BatchRun {
         uint8_t* qk = grow<uint8_t>(c.q_kind, std::max<uint64_t>(n, 1));
         double* qp = grow<double>(c.q_points, 24 * std::max<uint64_t>(n, 1));
         uint32_t* qfl = grow<uint32_t>(c.q_pflags, std::max<uint64_t>(n, 1));
-        launch_classify_keys(c, keys, n, c.last_nb, s.v0.as<double>(), s.v1.as<double>(), s.nv,
-                             s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp, qfl);
+        // K7: fused into the narrow phase's generation 0 (k_classify_gen0)
+        // unless the per-query separations need the records first
+        ClassifySrc src;
+        src.keys = keys;
+        src.n = n;
+        src.nb = c.last_nb;
+        src.v0 = s.v0.as<double>();
+        src.v1 = s.v1.as<double>();
+        src.nv = s.nv;
+        src.e = s.edges.as<uint32_t>();
+        src.ne = s.ne;
+        src.f = s.faces.as<uint32_t>();
+        src.kind_out = qk;
+        src.pts_out = qp;
+        src.qflags_out = qfl;
+        static const bool no_fuse_classify = std::getenv("CCDK_NO_FUSE_CLASSIFY") != nullptr;
+        const bool fuse_classify = n && !no_fuse_classify && cfg.min_sep_mode != CCDK_MINSEP_RELATIVE;
+        struct Pending { // never leave a dangling pending classification
+            Ctx& c;
+            ~Pending() { c.classify_pending = nullptr; }
+        } pending_guard { c };
+        if (fuse_classify)
+            c.classify_pending = &src;
+        else
+            launch_classify_keys(c, keys, n, c.last_nb, s.v0.as<double>(), s.v1.as<double>(), s.nv,
+                                 s.edges.as<uint32_t>(), s.ne, s.faces.as<uint32_t>(), qk, qp, qfl);
         double* seps = nullptr;
         if (cfg.min_sep_mode == CCDK_MINSEP_RELATIVE && n) {
             seps = grow<double>(c.q_sep, n);
@@ -646,6 +670,7 @@ struct BatchRun {
             narrow_batch(qk, qp, seps, qfl, 0, n, qoff);
         else
             ++narrow_batches; // an empty narrow run still counts as a batch
+        ensure_classified(c); // the records exist after the step whatever path ran
         CCDK_CUDA_CHECK(cudaEventSynchronize(e1));
         float ms = 0;
         CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));

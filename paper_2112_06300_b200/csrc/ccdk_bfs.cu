@@ -832,6 +832,105 @@ __global__ void __launch_bounds__(kClassifyBlock) k_classify_keys(
         out[i] = st[i];
 }
 
+// ---- K7 fused into generation 0: k_classify_keys'
+// gather and coalesced record write, then each lane evaluates its query's
+// root box [0,1]^3 from the coordinates still in its registers — k_gen0's
+// body without re-reading the 192-byte record it just wrote (411 MB at C4).
+// Generation 0's pruning snapshot is +inf and no query has split yet, so the
+// root's outcome depends only on the query: bit-identical to k_gen0.
+__global__ void __launch_bounds__(kClassifyBlock) k_classify_gen0(GenArgs a, ClassifySrc cs)
+{
+    __shared__ double stage[kClassifyBlock / 32][32 * 24];
+    const unsigned lane = threadIdx.x & 31;
+    double* st = stage[threadIdx.x >> 5];
+    const unsigned long long q = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    const unsigned long long q0 = q - lane;
+    if (q0 >= cs.n)
+        return; // warp-uniform
+    const bool valid = q < cs.n;
+    iv::RegPts P;
+    uint32_t qf = 0;
+    if (valid) {
+        const unsigned long long key = cs.keys[q];
+        const unsigned long long lo = key >> cs.nb;
+        const unsigned long long hi = key & ((1ull << cs.nb) - 1);
+        uint32_t pv[4];
+        uint8_t k;
+        if (lo < cs.nv) { // vertex-face: (p, t0, t1, t2)
+            const unsigned long long fi = hi - cs.nv - cs.ne;
+            pv[0] = static_cast<uint32_t>(lo);
+            pv[1] = cs.f[3 * fi];
+            pv[2] = cs.f[3 * fi + 1];
+            pv[3] = cs.f[3 * fi + 2];
+            k = CCDK_QUERY_VF;
+        } else { // edge-edge: (e0a, e0b, e1a, e1b)
+            const unsigned long long ea = lo - cs.nv, eb = hi - cs.nv;
+            pv[0] = cs.e[2 * ea];
+            pv[1] = cs.e[2 * ea + 1];
+            pv[2] = cs.e[2 * eb];
+            pv[3] = cs.e[2 * eb + 1];
+            k = CCDK_QUERY_EE;
+        }
+        cs.kind_out[q] = k;
+        bool fast = true;
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double x0 = cs.v0[3ull * pv[p] + c], x1 = cs.v1[3ull * pv[p] + c];
+                P.x[8 * c + 2 * p] = x0;
+                P.x[8 * c + 2 * p + 1] = x1;
+                st[24 * lane + 8 * c + 2 * p] = x0;
+                st[24 * lane + 8 * c + 2 * p + 1] = x1;
+                fast = fast && fabs(x0) <= iv::kFastLimit && fabs(x1) <= iv::kFastLimit;
+            }
+        qf = (k == CCDK_QUERY_EE ? iv::kKindEE : 0u) | (fast ? 0u : iv::kKindExact);
+        cs.qflags_out[q] = qf;
+    }
+    __syncwarp();
+    const unsigned long long nvalid = cs.n - q0 < 32 ? cs.n - q0 : 32;
+    double* out = cs.pts_out + 24 * q0;
+    for (unsigned i = lane; i < 24 * nvalid; i += 32)
+        out[i] = st[i];
+
+    // generation 0 (k_gen0) on the root
+    unsigned evals = 0, split_actions = 0;
+    SplitRec r[2];
+    r[0].dim = r[1].dim = -1;
+    if (valid) {
+        const iv::Box bx { 0.0, 1.0, 0.0, 1.0, 0.0, 1.0 };
+        const bool vf = !(qf & iv::kKindEE);
+        const double sep = a.sep ? a.sep[q] : a.sep_default;
+        double cand = 0;
+        bool zd = false, evald = false;
+        int dim = -1, act;
+        if (!(qf & iv::kKindExact)) {
+            act = iv::process_one<iv::Fast, iv::RegPts, true>(vf, P, bx, CUDART_INF, sep, a.cfg, cand, zd, dim,
+                                                              evald);
+        } else {
+            // rare (|x| > 2^1000): out of line, the register array goes by value
+            const iv::Outcome o = iv::process_exact<iv::RegPts>(vf, P, bx, CUDART_INF, sep, a.cfg);
+            act = o.act;
+            cand = o.cand;
+            zd = o.zdiag;
+            dim = o.dim;
+            evald = o.evaluated;
+        }
+        evals += evald;
+        if (act == iv::kCollision) {
+            record_collision(a, static_cast<unsigned>(q), cand, zd);
+        } else if (act == iv::kSplit) {
+            ++split_actions;
+            if (!a.cfg.no_zero_toi) // a root's only request of generation 0: always admitted
+                atomicAdd(&a.splits[q], 1ull);
+            r[0] = { dim, 0.0, 0.0, 0.0, 0ull };
+        }
+    }
+    append_splits(a, 1, lane, static_cast<unsigned>(valid ? q : 0), r);
+    warp_add(&a.sc->evaluations, evals);
+    warp_add(&a.sc->split_actions, split_actions);
+}
+
 // Reference-order query records (API input) -> internal order: (x0, x1) of
 // point p, component c at 8c + 2p.
 __global__ void k_records_to_internal(const double* __restrict__ ref, unsigned long long n,
@@ -879,19 +978,24 @@ T* grow(DevBuf& b, uint64_t n)
 // Build (or reuse) the generation graph:
 //   k_gen0 -> k_finish -> WHILE(cond) { k_generation -> k_finish }.
 // The condition defaults to 1 at every launch; k_finish clears it.
-void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_grid, unsigned fin_grid)
+void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_grid, unsigned fin_grid,
+                        const ClassifySrc* fused_classify)
 {
     GenGraph& G = c.gen_graph;
     struct Key {
         GenArgs a;
-        unsigned gen0_grid, gen_grid, fin_grid;
+        ClassifySrc cs;
+        unsigned gen0_grid, gen_grid, fin_grid, fused;
     } key;
     std::memset(&key, 0, sizeof key);
     key.a = a;
     key.a.cond = 0;
+    if (fused_classify)
+        key.cs = *fused_classify;
     key.gen0_grid = gen0_grid;
     key.gen_grid = gen_grid;
     key.fin_grid = fin_grid;
+    key.fused = fused_classify != nullptr;
     static_assert(sizeof(Key) <= sizeof(G.key), "graph key too large");
     if (G.exec && G.key_size == sizeof key && std::memcmp(G.key, &key, sizeof key) == 0) {
         CCDK_CUDA_CHECK(cudaGraphLaunch(G.exec, c.stream));
@@ -904,12 +1008,19 @@ void launch_generations(Ctx& c, GenArgs& a, unsigned gen0_grid, unsigned gen_gri
     GenArgs a0 = a; // generation 0 and its finish run outside the loop
     a0.cond = 0;
     a.cond = h;
-    void* params0[] = { &a0 };
+    ClassifySrc cs0 = fused_classify ? *fused_classify : ClassifySrc {};
+    void* params0[] = { &a0, &cs0 };
     void* params[] = { &a };
     cudaKernelNodeParams kp {};
-    kp.func = reinterpret_cast<void*>(k_gen0);
-    kp.gridDim = dim3(gen0_grid);
-    kp.blockDim = dim3(kGenBlock);
+    if (fused_classify) { // K7 + generation 0 in one kernel
+        kp.func = reinterpret_cast<void*>(k_classify_gen0);
+        kp.gridDim = grid_for(fused_classify->n, kClassifyBlock);
+        kp.blockDim = dim3(kClassifyBlock);
+    } else {
+        kp.func = reinterpret_cast<void*>(k_gen0);
+        kp.gridDim = dim3(gen0_grid);
+        kp.blockDim = dim3(kGenBlock);
+    }
     kp.kernelParams = params0;
     cudaGraphNode_t g0, f0;
     CCDK_CUDA_CHECK(cudaGraphAddKernelNode(&g0, G.graph, nullptr, 0, &kp));
@@ -992,6 +1103,13 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         cap = std::min<uint64_t>(cap, c.mem_probe_cap);
         cap = std::max<uint64_t>(cap, n);
     }
+    // K7 fused into generation 0 when this run covers exactly the records the
+    // pipeline left unwritten (ensure_classified writes them otherwise)
+    const ClassifySrc* fused_classify = nullptr;
+    if (c.classify_pending && c.classify_pending->kind_out == kind && c.classify_pending->n == n && cap >= n)
+        fused_classify = c.classify_pending;
+    else
+        ensure_classified(c);
     if (cap < n)
         return false;
     const uint64_t cap_pairs = std::max<uint64_t>(cap / 2, 1);
@@ -1049,14 +1167,19 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     if (c.exp && c.exp->pending)
         export_issue(c); // candidate export D2H runs under the generations
     static const bool no_graph = std::getenv("CCDK_NO_GRAPH") != nullptr;
+    if (fused_classify)
+        c.classify_pending = nullptr; // written by k_classify_gen0 below
     if (!no_graph) {
-        launch_generations(c, a, gen0_grid, gen_grid, fin_grid);
+        launch_generations(c, a, gen0_grid, gen_grid, fin_grid, fused_classify);
     } else {
         // direct launches (profilers cannot see kernel nodes under a
         // conditional node): batches of 8 generations, then a host check
         a.cond = 0;
         NarrowScalars* hs = static_cast<NarrowScalars*>(c.pin.ensure(sizeof(NarrowScalars)));
-        k_gen0<<<gen0_grid, kGenBlock, 0, s>>>(a);
+        if (fused_classify)
+            k_classify_gen0<<<grid_for(fused_classify->n, kClassifyBlock), kClassifyBlock, 0, s>>>(a, *fused_classify);
+        else
+            k_gen0<<<gen0_grid, kGenBlock, 0, s>>>(a);
         k_finish<<<fin_grid, 256, 0, s>>>(a);
         for (;;) {
             for (int g = 0; g < 8; ++g) {
@@ -1164,6 +1287,8 @@ void narrow_phase(Ctx& c, const NarrowIn& in, NarrowOut& out)
     cudaEvent_t e0 = c.events.get(EventPool::kNarrow), e1 = c.events.get(EventPool::kNarrow + 1);
     CCDK_CUDA_CHECK(cudaEventRecord(e0, c.stream));
     const bool bounded = in.queue_capacity != UINT64_MAX;
+    if (n > in.queue_capacity || n == 0)
+        ensure_classified(c); // no device run over these records: write them now
     if (n > 0 && n > in.queue_capacity) {
         // narrowphase.cpp:215-218: seeds alone exceed the capacity
         st.overflow = 1;
@@ -1259,6 +1384,16 @@ void launch_process(Ctx& c, const uint8_t* kind, const double* pts, const double
                                                       cfg.min_separation, action, cand_t, zdiag,
                                                       children, child_depth);
     CCDK_LAUNCH_CHECK();
+}
+
+void ensure_classified(Ctx& c)
+{
+    if (!c.classify_pending)
+        return;
+    const ClassifySrc cs = *c.classify_pending;
+    c.classify_pending = nullptr;
+    launch_classify_keys(c, cs.keys, cs.n, cs.nb, cs.v0, cs.v1, cs.nv, cs.e, cs.ne, cs.f, cs.kind_out, cs.pts_out,
+                         cs.qflags_out);
 }
 
 void launch_classify_keys(Ctx& c, const uint64_t* keys, uint64_t n, int nb, const double* v0,

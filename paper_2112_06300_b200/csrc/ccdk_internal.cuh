@@ -217,7 +217,7 @@ struct NarrowScalars {
 struct GenGraph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    unsigned char key[512];
+    unsigned char key[1024];
     size_t key_size = 0;
     GenGraph() = default;
     GenGraph(const GenGraph&) = delete;
@@ -281,6 +281,26 @@ struct BroadIn {
 void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out);
 
 // narrow phase (ccdk_narrow.cu)
+// Fused K7 + generation 0: the candidate keys and the scene a narrow run
+// classifies from itself (k_classify_gen0 writes the query records while it
+// evaluates the roots from registers).  Set in Ctx::classify_pending by the
+// pipeline; any path that cannot fuse calls ensure_classified() first.
+struct ClassifySrc {
+    const uint64_t* keys = nullptr;
+    uint64_t n = 0;
+    int nb = 0;
+    const double* v0 = nullptr;
+    const double* v1 = nullptr;
+    uint64_t nv = 0;
+    const uint32_t* e = nullptr;
+    uint64_t ne = 0;
+    const uint32_t* f = nullptr;
+    uint8_t* kind_out = nullptr;
+    double* pts_out = nullptr;
+    uint32_t* qflags_out = nullptr;
+};
+void ensure_classified(Ctx& c);
+
 struct NarrowIn {
     const uint8_t* kind = nullptr;   // device
     const double* points = nullptr;  // device, n*24, internal order (iv::GlobalPtsIL)
@@ -408,6 +428,8 @@ struct Ctx {
     bool last_keys_all = false; // fetch_pairs reads all_keys (pipeline) or pair_keys_sorted (API)
 
     PinnedBuf pin_scene;               // staging of pageable scene uploads
+    // fused classify (K7 into generation 0): records not yet written
+    const ClassifySrc* classify_pending = nullptr;
     // candidate export (ccdk_ccd_into)
     PairExport* exp = nullptr;
     DevBuf pair_ids;

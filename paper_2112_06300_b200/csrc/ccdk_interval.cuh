@@ -156,6 +156,19 @@ struct SmemPts { // internal order staged pair-major: pair k = 4c + p of lane l 
     }
 };
 
+struct RegPts { // internal order held in registers (compile-time indices only)
+    double x[24];
+    __device__ __forceinline__ double operator()(int e) const
+    {
+        const int t = e / 12, r = e % 12;
+        return x[8 * (r % 3) + 2 * (r / 3) + t];
+    }
+    __device__ __forceinline__ double2 pair(int pt, int c) const
+    {
+        return make_double2(x[8 * c + 2 * pt], x[8 * c + 2 * pt + 1]);
+    }
+};
+
 // One component c of evaluate_box: the hull `rng` of the 8 corners and the
 // component's contribution to the three influences.
 template <class W, class Pts>
@@ -253,7 +266,7 @@ enum : int { kPruned = 0, kCollision = 1, kSplit = 2 };
 
 // process_interval (narrowphase.cpp:134-187).  Returns the action; for Split
 // `dim` is the bisection dimension (0 t, 1 u, 2 v).
-template <class W, class Pts>
+template <class W, class Pts, bool kUnrollC = false>
 __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
                                            double t_star, double d, const Cfg& cfg,
                                            double& cand_t, bool& zdiag, int& dim,
@@ -266,25 +279,36 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
         return kPruned;
     if (vf && __dadd_rn(b.ulo, b.vlo) > 1.0)
         return kPruned;
-    // Components one at a time (rolled loop: a third of the code, so the hot
-    // loop stays in the instruction cache).  A component whose range misses
-    // the tolerance cube prunes the box whatever the others hold, so the loop
+    // Components one at a time.  A component whose range misses the
+    // tolerance cube prunes the box whatever the others hold, so the loop
     // exits early; otherwise the inside test, max width and influences are
-    // reduced on the fly (all order-independent).
+    // reduced on the fly (all order-independent).  The loop stays rolled (a
+    // third of the code, so a hot loop stays in the instruction cache) unless
+    // kUnrollC: coordinates held in a register array need compile-time
+    // component indices.
     Eval ev;
     ev.infl[0] = ev.infl[1] = ev.infl[2] = 0.0;
     evaluated = true;
     bool inside = true;
     double wmax = 0.0;
-#pragma unroll 1
-    for (int c = 0; c < 3; ++c) {
+    auto comp = [&](int c) -> bool { // true: the component prunes the box
         I rng;
         component<W, Pts>(vf, P, b, c, rng, ev.infl);
         if (rng.lo > d || rng.hi < -d)
-            return kPruned;
+            return true;
         inside = inside && rng.lo >= -d && rng.hi <= d;
         const double w = __dsub_rn(rng.hi, rng.lo);
         wmax = c == 0 ? w : smax(wmax, w);
+        return false;
+    };
+    if constexpr (kUnrollC) {
+        if (comp(0) || comp(1) || comp(2))
+            return kPruned;
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < 3; ++c)
+            if (comp(c))
+                return kPruned;
     }
     const bool force_zero = cfg.no_zero_toi && b.tlo == 0.0;
     if (!force_zero) {
