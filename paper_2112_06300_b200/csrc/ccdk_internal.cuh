@@ -10,6 +10,8 @@
 #include <mutex>
 #include <stdexcept>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <future>
 #include <string>
 #include <thread>
@@ -165,6 +167,92 @@ struct EventPool {
         }
         return ev[i];
     }
+};
+
+// Persistent host helper threads of a context (staging copies of pageable
+// uploads): spawning threads per call cost more than the copies they share.
+// run(f, k) runs f on k helpers and the caller and returns when all are done.
+class HostPool {
+public:
+    HostPool() = default;
+    HostPool(const HostPool&) = delete;
+    HostPool& operator=(const HostPool&) = delete;
+    ~HostPool()
+    {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_)
+            t.join();
+    }
+    template <class F>
+    void run(F&& f, unsigned helpers)
+    {
+        start(std::forward<F>(f), helpers);
+        (*task_)();
+        wait();
+    }
+    // run f on `helpers` threads and return at once; wait() joins them
+    template <class F>
+    void start(F&& f, unsigned helpers)
+    {
+        ensure(helpers);
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            task_store_ = std::function<void()>(std::forward<F>(f));
+            task_ = &task_store_;
+            want_ = helpers;
+            busy_ = helpers;
+            ++gen_;
+        }
+        cv_.notify_all();
+    }
+    void wait()
+    {
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [this] { return busy_ == 0; });
+        task_ = nullptr;
+    }
+
+private:
+    void ensure(unsigned n)
+    {
+        while (threads_.size() < n) {
+            const unsigned id = static_cast<unsigned>(threads_.size());
+            threads_.emplace_back([this, id] { loop(id); });
+        }
+    }
+    void loop(unsigned id)
+    {
+        unsigned long long seen = 0;
+        for (;;) {
+            std::function<void()>* t;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && id < want_); });
+                if (stop_)
+                    return;
+                seen = gen_;
+                t = task_;
+            }
+            (*t)();
+            {
+                std::lock_guard<std::mutex> lk(m_);
+                --busy_;
+            }
+            done_.notify_one();
+        }
+    }
+    std::vector<std::thread> threads_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::function<void()>* task_ = nullptr;
+    std::function<void()> task_store_;
+    unsigned want_ = 0, busy_ = 0;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
 };
 
 // Device-side scene (canonical slot order V, E, F; aabb.cpp:79-105).
@@ -428,6 +516,7 @@ struct Ctx {
     bool last_keys_all = false; // fetch_pairs reads all_keys (pipeline) or pair_keys_sorted (API)
 
     PinnedBuf pin_scene;               // staging of pageable scene uploads
+    HostPool host_pool;                // helper threads of the staging copies
     // fused classify (K7 into generation 0): records not yet written
     const ClassifySrc* classify_pending = nullptr;
     // candidate export (ccdk_ccd_into)

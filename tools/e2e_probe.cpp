@@ -59,6 +59,12 @@ int main()
         auto i = Clock::now();
         const ccdkit::CcdReport full = ccdkit::ccd(s, [] { ccdkit::PipelineConfig p; p.inflation = 0.01; return p; }());
         auto j = Clock::now();
+        ccdk_scene_upload(ctx, v0, v1, nv, e, ne, f, nf);
+        auto k2 = Clock::now();
+        ccdk_report rr {};
+        ccdk_ccd_resident(ctx, &cfg, 0, 1, &rr);
+        auto l2 = Clock::now();
+        std::printf("  resident: upload %.2f ms, step %.2f ms (device %.2f)\n", ms(j, k2), ms(k2, l2), rr.ms_total);
         std::printf("pageable H2D %.2f | ccdk_ccd %.2f (device total %.2f) | into+noop %.2f | into+fill %.2f | host fill %.2f | ccdkit::ccd %.2f ms (n=%llu)\n",
                     ms(a, b), ms(b, c), r.ms_total, ms(c, d), ms(d, g), ms(h, i), ms(i, j), (unsigned long long)r.candidate_count);
     }
