@@ -581,7 +581,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": bench_config(args.workload, k),
         "parallelism": f"sweep-range shards x{world}"
-                       + (", candidates rebalanced by count (all_to_all)" if rebalance else "")
+                       + (", candidates interleaved across ranks (one all_to_all)" if rebalance else "")
                        + ", allreduce(min)",
         "narrow_queries_per_s": queries / (narrow_ms * 1e-3) if narrow_ms > 0 else None,
         "candidates": candidates, "queries": queries, "toi": gtoi,
