@@ -147,6 +147,21 @@ def load_peaks():
         return {}
 
 
+def measure_fp64_peak():
+    """fp64 roofline denominator measured on this box before the timed region:
+    dependent-free DADD throughput over every SM (tools/ubench_fp64 --peak;
+    MEASURED_PEAKS.json carries only HBM and bf16).  None if unavailable."""
+    import subprocess
+    exe = os.path.join(ROOT, "tools", "ubench_fp64")
+    if not os.path.exists(exe):
+        return None
+    try:
+        r = subprocess.run([exe, "--peak"], capture_output=True, text=True, timeout=60)
+        return json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
+    except Exception:
+        return None
+
+
 def load_traffic():
     """ncu dram byte counts per launch / per step (profiles/traffic_r0N.json,
     newest round first)."""
@@ -405,6 +420,7 @@ def run_ours(args):
     cfg = ck.PipelineConfig(inflation=0.01)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     clocks = ClockSampler(local)  # NVML initialised outside the timed region
+    fp64_measured = measure_fp64_peak() if rank == 0 else None
 
     def barrier():
         if world > 1:
@@ -524,7 +540,16 @@ def run_ours(args):
     # 62.7 ops/SM/clk (tools/ubench_fp64.cu, profiles/r01_ubench_fp64.txt; the
     # nominal 64 lanes x 148 SMs); MEASURED_PEAKS.json carries only HBM and bf16
     sm_clk = clk.get("sm_mhz") or sm_max
-    fp64_peak = 148 * 62.7 * sm_clk * 1e6 / 1e12
+    if fp64_measured:
+        fp64_peak = fp64_measured["dadd_tflops"]
+        fp64_src = (f"measured in this run before the timed region: tools/ubench_fp64 --peak, dependent-free DADD "
+                    f"over all {fp64_measured['sms']} SMs = {fp64_measured['dadd_tflops']:.2f} T ops/s "
+                    f"({fp64_measured['ops_per_sm_clk_at_max']:.1f} ops/SM/clk at the {fp64_measured['max_clock_mhz']} "
+                    f"MHz max clock); bound is the fp64 pipe (bit-exact fp64 interval arithmetic, no FMA, no tensor cores)")
+    else:
+        fp64_peak = 148 * 62.7 * sm_clk * 1e6 / 1e12
+        fp64_src = ("fallback: DADD rate 62.7/SM/clk measured in round 1 (profiles/r01_ubench_fp64.txt) x 148 SMs x "
+                    "sampled SM clock")
     narrow_tf = flops / (d["ms_narrow"] * 1e-3) / 1e12 if d["ms_narrow"] > 0 else 0.0
     k = scene.primitive_count()
     sweep_bytes = 40.0 * k + 8.0 * rep.candidate_count
@@ -535,9 +560,7 @@ def run_ours(args):
                 "bound": "fp64", "achieved": narrow_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": narrow_tf / fp64_peak, "traffic": traffic.get("k_generation_bytes_per_launch"),
                 "traffic_note": traffic.get("k_generation_note", traffic.get("note")),
-                "peak_source": "measured DADD rate 62.7/SM/clk (profiles/r01_ubench_fp64.txt) x 148 SMs x "
-                               "sampled SM clock; bound is the fp64 pipe (neither HBM nor tensor cores: "
-                               "bit-exact fp64 interval arithmetic, no FMA)",
+                "peak_source": fp64_src,
                 "algorithmic": f"F = 339*E + 96*S, E={d['evaluations']}, S={d['split_actions']}"}
     roofline_sweep = {"kernel": "K4+K5 sweep stage (slab set-up or run ends, heavy segments, row / short / heavy "
                                 "sweep kernels)", "bound": "hbm",

@@ -3,6 +3,7 @@
 // independent chains per thread (ILP 8) so it measures throughput, not latency.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false tools/ubench_fp64.cu -o /tmp/ub
 #include <cstdio>
+#include <string>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -109,8 +110,46 @@ void run(const char* name, double* out)
            ops / (ms * 1e-3) / 1e9, per_sm_clk, clk / 1000);
 }
 
-int main()
+// --peak: the fp64 roofline denominator bench.py uses, measured on the box it
+// runs on: dependent-free DADD throughput over every SM, one JSON line.
+int peak_json()
 {
+    double* out;
+    cudaMalloc(&out, 4096 * sizeof(double));
+    int sms = 0, clk = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    const int blocks = sms * 8, threads = 256;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        k<0><<<blocks, threads>>>(out, 1.0); // warm
+        cudaEventRecord(a);
+        for (int r = 0; r < 5; ++r)
+            k<0><<<blocks, threads>>>(out, 1.0);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double ops = 5.0 * blocks * threads * (double)ITERS * ILP;
+        const double rate = ops / (ms * 1e-3);
+        if (rate > best)
+            best = rate;
+    }
+    if (cudaGetLastError() != cudaSuccess)
+        return 1;
+    printf("{\"dadd_ops_per_s\": %.6e, \"dadd_tflops\": %.4f, \"sms\": %d, \"max_clock_mhz\": %d, "
+           "\"ops_per_sm_clk_at_max\": %.3f}\n",
+           best, best / 1e12, sms, clk / 1000, best / sms / (clk * 1e3));
+    return 0;
+}
+
+int main(int argc, char** argv)
+{
+    if (argc > 1 && std::string(argv[1]) == "--peak")
+        return peak_json();
     double* out;
     cudaMalloc(&out, 4096 * sizeof(double));
     run<0>("DADD", out);
