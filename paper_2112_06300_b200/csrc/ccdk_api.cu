@@ -553,6 +553,7 @@ struct BatchRun {
     float ms_sort = 0, ms_sweep = 0, ms_pairsort = 0, ms_classify = 0, ms_narrow = 0;
     int axis = 0;
     uint64_t slabs = 0, slab_entries = 0;
+    bool check_build_error = false; // the box build's flag, checked by the first broad phase
 
     // broad_batch (pipeline.cpp:140-174): halve the sweep range while the
     // candidates exceed the budget's pair capacity
@@ -572,18 +573,25 @@ struct BatchRun {
         // the axis matters only if the budget can force range halving
         bi.exact_axis = cap_pairs < k * (k - 1) / 2;
         bi.allow_slab = allow_slab;
+        bi.check_build_error = check_build_error;
+        check_build_error = false; // checked at this broad phase's first read-back
+        bi.defer_collect = true;   // times / axis read after the narrow phase's own sync
         BroadOut bo;
         broad_phase(c, bi, bo);
         launches += bo.launches;
         pair_tests += bo.pair_tests;
-        ms_sort += bo.ms_axis_sort;
-        ms_sweep += bo.ms_sweep;
-        ms_pairsort += bo.ms_pairsort;
-        axis = bo.axis;
         slabs = bo.slab_count;
         slab_entries = bo.slab_entries;
+        auto collect = [&] {
+            broad_collect(c, bo);
+            ms_sort += bo.ms_axis_sort;
+            ms_sweep += bo.ms_sweep;
+            ms_pairsort += bo.ms_pairsort;
+            axis = bo.axis;
+        };
         if (shard_count > 1 && bo.slab_mode && bo.n_pairs > cap_pairs) {
             // budget halving is defined on sorted positions: redo this shard 1-D
+            collect();
             broad_batch(begin, end, shard_rank, shard_count, false);
             return;
         }
@@ -592,6 +600,7 @@ struct BatchRun {
             end = bo.range_hi;
         }
         if (bo.n_pairs > cap_pairs && end - begin > 1) {
+            collect(); // before the next broad phase reuses the events
             const uint64_t mid = begin + (end - begin) / 2;
             broad_batch(begin, mid);
             broad_batch(mid, end);
@@ -602,6 +611,7 @@ struct BatchRun {
             export_begin(c, c.pair_keys_sorted.as<uint64_t>(), bo.n_pairs, s.nv, s.ne, true);
         ++broad_batches;
         process_keys(c.pair_keys_sorted.as<uint64_t>(), bo.n_pairs);
+        collect();
     }
 
     // The rest of a broad batch on canonical pair keys (lo << nb | hi over
@@ -653,13 +663,17 @@ struct BatchRun {
             launch_min_seps(c, qk, qp, n, cfg, seps, true);
             ++launches;
         }
-        unsigned long long nvf = 0;
+        // the VF count goes to pinned memory and is read after the narrow
+        // phase's own sync (a pageable read-back here would drain the queue
+        // before the narrow phase is even enqueued)
+        unsigned long long* nvf_h = static_cast<unsigned long long*>(c.pin_axis.ensure(64)) + 4;
+        *nvf_h = 0;
         if (n) {
             auto* ctr = c.counters.as<DevCounters>();
             k_count_vf<<<1, 1, 0, c.stream>>>(reinterpret_cast<const unsigned long long*>(keys), n,
                                               c.last_nb, s.nv, &ctr->misc[2]);
             CCDK_LAUNCH_CHECK();
-            d2h(c, &nvf, &ctr->misc[2], 8);
+            d2h(c, nvf_h, &ctr->misc[2], 8);
             launches += 2;
         }
         CCDK_CUDA_CHECK(cudaEventRecord(e1, c.stream));
@@ -675,7 +689,7 @@ struct BatchRun {
         float ms = 0;
         CCDK_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
         ms_classify += ms;
-        vf += nvf;
+        vf += *nvf_h;
     }
 
     void grow_results(uint64_t nq)
@@ -760,7 +774,7 @@ void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_
     launch_build_boxes(c, s.v0.as<double>(), s.v1.as<double>(), s.nv, s.edges.as<uint32_t>(), s.ne,
                        s.faces.as<uint32_t>(), s.nf, cfg.inflation, bmin, bmax, vids);
     CCDK_CUDA_CHECK(cudaEventRecord(ev[1], st));
-    if (k) {
+    if (k && k < 2) { // no broad phase to fold the check into
         auto* ctr = c.counters.as<DevCounters>();
         unsigned long long err = 0;
         d2h(c, &err, &ctr->error, 8);
@@ -769,6 +783,7 @@ void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_
             throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
     }
     BatchRun run { c, cfg, s, k, cap_pairs };
+    run.check_build_error = k >= 2; // at the broad phase's first read-back (one round trip fewer)
     run.bmin = bmin;
     run.bmax = bmax;
     run.vids = vids;

@@ -1123,10 +1123,15 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         });
         uint32_t tail[2];
         SlabParams hp {};
+        unsigned long long berr = ~0ull;
         CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[0], eoff + k - 1, 4, cudaMemcpyDeviceToHost, s));
         CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[1], cnt + k - 1, 4, cudaMemcpyDeviceToHost, s));
         CCDK_CUDA_CHECK(cudaMemcpyAsync(&hp, P, sizeof hp, cudaMemcpyDeviceToHost, s));
+        if (in.check_build_error)
+            CCDK_CUDA_CHECK(cudaMemcpyAsync(&berr, &ctr->error, 8, cudaMemcpyDeviceToHost, s));
         CCDK_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (berr != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
         const uint64_t E = static_cast<uint64_t>(tail[0]) + tail[1];
         // copies of wide boxes multiply the entries; beyond 4 k the 1-D sweep wins
         if (hp.ok && E <= 4 * k) {
@@ -1243,6 +1248,8 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[0], off + rows - 1, 4, cudaMemcpyDeviceToHost, s));
         CCDK_CUDA_CHECK(cudaMemcpyAsync(&tail[1], nseg + rows - 1, 4, cudaMemcpyDeviceToHost, s));
         read_ctr();
+        if (in.check_build_error && host_ctr[3] != ~0ull)
+            throw Error(CCDK_INVALID_INPUT, "round_down_reduced: non-finite input");
         const uint64_t total = static_cast<uint64_t>(tail[0]) + tail[1];
         if (total > seg_cap) {
             seg_cap = total;
@@ -1349,17 +1356,28 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
         }
     }
     CCDK_CUDA_CHECK(cudaEventRecord(ev[3], s));
-    int axis[4] = { 0, 0, 0, 0 };
-    CCDK_CUDA_CHECK(cudaMemcpyAsync(axis, d_axis, sizeof axis, cudaMemcpyDeviceToHost, s));
+    int* axis_h = static_cast<int*>(c.pin_axis.ensure(64)); // words 0-3 axis, 8-byte word 4: the step's VF count
+    CCDK_CUDA_CHECK(cudaMemcpyAsync(axis_h, d_axis, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    out.n_pairs = n_pairs;
+    c.last_n_pairs = n_pairs;
+    if (!in.defer_collect)
+        broad_collect(c, out);
+}
+
+// Stage times and the axis of the last broad phase (waits for its end).
+void broad_collect(Ctx& c, BroadOut& out)
+{
+    cudaEvent_t ev[4];
+    for (int i = 0; i < 4; ++i)
+        ev[i] = c.events.get(EventPool::kBroad + i);
     CCDK_CUDA_CHECK(cudaEventSynchronize(ev[3]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_axis_sort, ev[0], ev[1]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_sweep, ev[1], ev[2]));
     CCDK_CUDA_CHECK(cudaEventElapsedTime(&out.ms_pairsort, ev[2], ev[3]));
+    const int* axis = c.pin_axis.as<int>();
     out.axis = axis[0];
     out.axis_near_tie = axis[1] != 0;
     out.axis_serial = axis[2] != 0;
-    out.n_pairs = n_pairs;
-    c.last_n_pairs = n_pairs;
 }
 
 } // namespace ccdk

@@ -141,6 +141,11 @@ struct PinnedBuf {
         }
         return p;
     }
+    template <typename T>
+    T* as() const
+    {
+        return static_cast<T*>(p);
+    }
 };
 
 // Timing events, created once per context (creating/destroying events per
@@ -365,7 +370,13 @@ struct BroadIn {
     // is observable through choose_axis, StqStats and SweepRange slices)
     bool exact_axis = true;
     bool allow_slab = true; // slab-mode sweep permitted (full range, no StqStats)
+    // the box build's non-finite flag (DevCounters::error) is checked at the
+    // broad phase's first read-back instead of its own host round trip
+    bool check_build_error = false;
+    // leave the stage times / axis for broad_collect() (the caller syncs later)
+    bool defer_collect = false;
 };
+void broad_collect(Ctx& c, BroadOut& out);
 void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out);
 
 // narrow phase (ccdk_narrow.cu)
@@ -516,6 +527,7 @@ struct Ctx {
     bool last_keys_all = false; // fetch_pairs reads all_keys (pipeline) or pair_keys_sorted (API)
 
     PinnedBuf pin_scene;               // staging of pageable scene uploads
+    PinnedBuf pin_axis;                // the broad phase's axis words (read back asynchronously)
     HostPool host_pool;                // helper threads of the staging copies
     // fused classify (K7 into generation 0): records not yet written
     const ClassifySrc* classify_pending = nullptr;
