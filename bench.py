@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rebalance", choices=["auto", "on", "off"], default="auto",
-                    help="multi-GPU narrow-phase load balance by candidate count (auto: on when N > 1)")
+                    help="multi-GPU candidate exchange (interleaved, one all_to_all) before the narrow phase "
+                         "(auto: off — the slab-mode SweepRange shards balance C4 on their own)")
     ap.add_argument("--c5-queries", type=int, default=10_000_000,
                     help="narrow-phase-only leg (BASELINE config 5); 0 disables")
     ap.add_argument("--c5-steps", type=int, default=3)
@@ -410,7 +411,13 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2112_06300_b200 import abi, ccdkit as ck, native, scenes
     from paper_2112_06300_b200.multigpu import RebalancedCcd, ShardedCcd
-    rebalance = args.rebalance == "on" or (args.rebalance == "auto" and world > 1)
+    # auto = the SweepRange shards alone: with the slab-mode sweep each rank's
+    # entry-row shard carries a balanced share of narrow work on this scene
+    # (profiles/r02_predict_scaling_C4.json: N = 8 step 2.63 ms sharded vs
+    # 2.70 ms interleaved, before the rebalance's extra host round trips,
+    # measured +0.6 ms at N = 1); --rebalance on exchanges candidates for
+    # skewed scenes
+    rebalance = args.rebalance == "on"
     Step = RebalancedCcd if rebalance else ShardedCcd
 
     stream = torch.cuda.Stream()
