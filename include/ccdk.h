@@ -38,7 +38,8 @@
 extern "C" {
 #endif
 
-#define CCDK_ABI_VERSION 2 /* 2: ccdk_report gained sweep_slabs, sweep_entries; ccdk_ccd_into */
+#define CCDK_ABI_VERSION 2 /* 2: ccdk_report gained sweep_slabs, sweep_entries; ccdk_ccd_into,
+                              ccdk_run_batched */
 
 #if defined(__GNUC__)
 #define CCDK_API __attribute__((visibility("default")))
@@ -265,6 +266,22 @@ CCDK_API int ccdk_ccd_into(ccdk_ctx* ctx, const double* v0, const double* v1, ui
                            const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
                            const ccdk_pipeline_cfg* cfg, ccdk_report* report, ccdk_pairs_sink sink,
                            void* user);
+
+/* run_batched (pipeline.hpp:78-80, pipeline.cpp:179-215) on a caller's box
+ * list: k boxes as min_corner/max_corner [k][3] floats and owners (kind,
+ * index), any order, duplicates allowed.  No box build (cfg->inflation is
+ * not used); broad batches halve sorted positions for stq/sap and raw box
+ * positions for bf, as the reference does.  Every owner must name an
+ * existing primitive (CCDK_INVALID_INPUT otherwise; the reference would
+ * index out of bounds).  The scene is validated like ccdk_ccd's.  Candidates
+ * go to `sink` as in ccdk_ccd_into (sink may be NULL: they stay in the
+ * context for ccdk_fetch_pairs); report->broad_batches and
+ * report->batch_count are BatchTrace's broad_batches and narrow_batches. */
+CCDK_API int ccdk_run_batched(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
+                              const uint32_t* edges, uint64_t ne, const uint32_t* faces, uint64_t nf,
+                              const float* min_corner, const float* max_corner, const uint8_t* owner_kind,
+                              const uint32_t* owner_index, uint64_t k, const ccdk_pipeline_cfg* cfg,
+                              ccdk_report* report, ccdk_pairs_sink sink, void* user);
 
 /* ccd_no_zero_toi (pipeline.hpp:82-85, pipeline.cpp:234-256): requires
  * cfg->narrow.no_zero_toi; a separated run, then on an exact-zero ToI a

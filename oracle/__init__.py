@@ -218,6 +218,20 @@ class _Cpu:
         return rep, pairs
 
     # ---- reference-only helpers
+    def run_batched(self, s, boxes, cfg):
+        """run_batched (pipeline.cpp:179-215) on a caller's box list.
+        Returns (report, pairs (n,2) u64, broad_batches, narrow_batches)."""
+        mn, mx, kind, idx = [np.ascontiguousarray(a) for a in boxes]
+        rep = abi.Report()
+        pp, bb, nb = P_U64(), C.c_uint64(), C.c_uint64()
+        self._check(self.lib.ref_run_batched(
+            ptr(s.vertices_t0, C.c_double), ptr(s.vertices_t1, C.c_double), C.c_uint64(s.nv),
+            ptr(s.edges, C.c_uint32), C.c_uint64(s.ne), ptr(s.faces, C.c_uint32), C.c_uint64(s.nf),
+            ptr(mn, C.c_float), ptr(mx, C.c_float), ptr(kind, C.c_uint8), ptr(idx, C.c_uint32),
+            C.c_uint64(mn.shape[0]), C.byref(cfg), C.byref(rep), C.byref(bb), C.byref(nb), C.byref(pp)))
+        pairs = self._take(pp, 2 * rep.candidate_count, np.uint64).reshape(-1, 2)
+        return rep, pairs, bb.value, nb.value
+
     def make_scene(self, name, *args):
         from paper_2112_06300_b200.scenes import SceneStep
         v0, v1, e, f = P_F64(), P_F64(), P_U32(), P_U32()

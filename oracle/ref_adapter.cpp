@@ -403,6 +403,40 @@ int ref_ccd(const double* v0, const double* v1, uint64_t nv, const uint32_t* e, 
     });
 }
 
+// run_batched (pipeline.cpp:179-215) on a caller's box list; the trace's
+// counters go to broad_batches / narrow_batches.
+int ref_run_batched(const double* v0, const double* v1, uint64_t nv, const uint32_t* e, uint64_t ne,
+                    const uint32_t* f, uint64_t nf, const float* mn, const float* mx, const uint8_t* kind,
+                    const uint32_t* index, uint64_t k, const ccdk_pipeline_cfg* cfg, ccdk_report* rep,
+                    uint64_t* broad_batches, uint64_t* narrow_batches, uint64_t** pairs)
+{
+    return guard([&] {
+        const SceneStep s = make_scene(v0, v1, nv, e, ne, f, nf);
+        const std::vector<Aabb> boxes = make_boxes(mn, mx, kind, index, k);
+        const PipelineConfig pc = make_pcfg(cfg);
+        BatchTrace trace;
+        CcdReport r;
+        const ToiResult t = run_batched(s, boxes, pc, trace, &r);
+        std::memset(rep, 0, sizeof *rep);
+        rep->toi = t.toi;
+        rep->tolerance_hit = t.tolerance_hit;
+        rep->zero_toi_diagnostic = t.zero_toi_diagnostic;
+        rep->candidate_count = r.candidate_count;
+        rep->query_count = r.query_count;
+        rep->batch_count = r.batch_count;
+        rep->tracked_peak_bytes = r.tracked_peak_bytes;
+        *broad_batches = trace.broad_batches;
+        *narrow_batches = trace.narrow_batches;
+        std::vector<uint64_t> flat;
+        flat.reserve(2 * r.candidates.size());
+        for (const auto& p : r.candidates) {
+            flat.push_back(pack_id(p.left));
+            flat.push_back(pack_id(p.right));
+        }
+        *pairs = dup(flat);
+    });
+}
+
 int ref_make_cloth_scene(uint64_t nx, uint64_t ny, double jitter, double drop,
                          uint64_t seed, double** v0, double** v1, uint64_t* nv,
                          uint32_t** e, uint64_t* ne, uint32_t** f, uint64_t* nf)

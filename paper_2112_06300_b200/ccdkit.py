@@ -159,6 +159,13 @@ class CcdReport:
     device: dict = field(default_factory=dict)
 
 
+@dataclass
+class BatchTrace:
+    """BatchTrace (pipeline.hpp:69-72): batches run_batched actually ran."""
+    broad_batches: int = 0
+    narrow_batches: int = 0
+
+
 def _ctx(ctx):
     return ctx if ctx is not None else default_context()
 
@@ -436,6 +443,46 @@ def ccd(scene: SceneStep, cfg: PipelineConfig | None = None, want_candidates: bo
             if r.candidate_count:
                 check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
     return _report(r, pairs)
+
+
+def run_batched(scene: SceneStep, boxes: Boxes, cfg: PipelineConfig, trace: BatchTrace,
+                report: CcdReport | None = None, ctx=None) -> ToiResult:
+    """run_batched (pipeline.hpp:78-80, pipeline.cpp:179-215) on a caller's box
+    list (any order, duplicates allowed): budget-batched broad + narrow phase.
+    Accumulates into `trace`; updates only the report fields the reference's
+    run_batched writes (toi, counts, batch_count, BP / SO/CD / NP, the peak
+    bytes as a max, candidates)."""
+    c = _ctx(ctx)
+    if scene.vertices_t0.shape != scene.vertices_t1.shape:
+        raise InvalidInput(abi.INVALID_INPUT, "vertex snapshots differ in length")
+    mn = np.ascontiguousarray(boxes.min_corner, np.float32).reshape(-1, 3)
+    mx = np.ascontiguousarray(boxes.max_corner, np.float32).reshape(-1, 3)
+    kd = np.ascontiguousarray(boxes.owner_kind, np.uint8)
+    ix = np.ascontiguousarray(boxes.owner_index, np.uint32)
+    r = abi.Report()
+    ccfg = cfg.to_c()
+    with c.lock:
+        check(lib().ccdk_run_batched(c.h, p(scene.vertices_t0, P_F64), p(scene.vertices_t1, P_F64), scene.nv,
+                                     p(scene.edges, P_U32), scene.ne, p(scene.faces, P_U32), scene.nf,
+                                     p(mn, P_F32), p(mx, P_F32), p(kd, P_U8), p(ix, P_U32), len(kd),
+                                     C.byref(ccfg), C.byref(r), None, None))
+        pairs = None
+        if report is not None:
+            pairs = np.empty((r.candidate_count, 2), np.uint64)
+            if r.candidate_count:
+                check(lib().ccdk_fetch_pairs(c.h, p(pairs, P_U64)))
+    trace.broad_batches += int(r.broad_batches)
+    trace.narrow_batches += int(r.batch_count)
+    toi = ToiResult(r.toi, bool(r.tolerance_hit), bool(r.zero_toi_diagnostic))
+    if report is not None:
+        report.toi = toi
+        report.candidate_count = int(r.candidate_count)
+        report.query_count = int(r.query_count)
+        report.batch_count = max(1, trace.narrow_batches)
+        report.per_stage_times.update({"BP": r.t_bp, "SO/CD": r.t_socd, "NP": r.t_np})
+        report.tracked_peak_bytes = max(report.tracked_peak_bytes, int(r.tracked_peak_bytes))
+        report.candidates = pairs
+    return toi
 
 
 def ccd_no_zero_toi(scene: SceneStep, cfg: PipelineConfig, want_candidates: bool = True,

@@ -143,16 +143,19 @@ __global__ void k_rank_flags(const unsigned long long* skeys, unsigned long long
     flag[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1u : 0u;
 }
 
-// Gather boxes into owner order: SoA corners, vertex triple + dense rank, raw
-// position; owner tables by rank.  Owner indices are range-checked (the
-// reference's share_vertex would index out of bounds).
+// Gather boxes into owner order: SoA corners, vertex triple + rank, raw
+// position.  Owner indices are range-checked (the reference's share_vertex
+// would index out of bounds).  Ranks are dense over the distinct owners, with
+// owner tables by rank (general broad phase), or — canon, run_batched — the
+// owner's canonical slot (V, then E, then F), which the pipeline's classify
+// and candidate export decode directly; vertex indices must then be < nv.
 __global__ void k_gather_general(const float* mn, const float* mx, const uint8_t* kind,
                                  const uint32_t* index, const uint32_t* order,
                                  const uint32_t* rank_incl, unsigned long long k,
                                  unsigned long long nv, const uint32_t* e, unsigned long long ne,
                                  const uint32_t* f, unsigned long long nf, float* bmin,
                                  float* bmax, uint4* vids, uint32_t* raw, uint8_t* own_kind,
-                                 uint32_t* own_index, unsigned long long* err)
+                                 uint32_t* own_index, unsigned long long* err, bool canon)
 {
     const unsigned long long s = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (s >= k)
@@ -164,11 +167,14 @@ __global__ void k_gather_general(const float* mn, const float* mx, const uint8_t
     }
     const uint8_t kd = kind[r];
     const uint32_t ix = index[r];
-    const uint32_t rank = rank_incl[s] - 1;
+    uint32_t rank = rank_incl[s] - 1;
+    if (canon)
+        rank = static_cast<uint32_t>(ix + (kd == CCDK_KIND_EDGE ? nv : kd == CCDK_KIND_FACE ? nv + ne : 0));
     uint4 w = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, rank);
     bool bad = false;
     if (kd == CCDK_KIND_VERTEX) {
         w.x = ix; // share_vertex compares the index itself (scene.cpp:58-60)
+        bad = canon && ix >= nv;
     } else if (kd == CCDK_KIND_EDGE) {
         if (ix < ne) {
             w.x = e[2ull * ix];
@@ -191,8 +197,10 @@ __global__ void k_gather_general(const float* mn, const float* mx, const uint8_t
         atomicMin(err, s);
     vids[s] = w;
     raw[s] = static_cast<uint32_t>(r);
-    own_kind[rank] = kd;
-    own_index[rank] = ix;
+    if (!canon) {
+        own_kind[rank] = kd;
+        own_index[rank] = ix;
+    }
 }
 
 __global__ void k_aos_to_soa(const float* mn, const float* mx, unsigned long long k, float* bmin,
@@ -531,6 +539,77 @@ void export_finish(Ctx& c)
         throw Error(CCDK_OOM, "ccdk_ccd_into: the candidate sink failed");
 }
 
+// A caller's box list on the device in owner order (slot order = the sort's
+// tie-break, broadphase.cpp:22-34): upload, sort by owner, gather.  Owners
+// are range-checked here (one round trip); nranks < k means duplicate owners.
+struct UserBoxes {
+    float* bmin = nullptr;
+    float* bmax = nullptr;
+    uint4* vids = nullptr;
+    uint32_t* raw = nullptr;
+    uint64_t nranks = 0;
+};
+
+// run_batched's box list as the caller holds it (host AoS split into arrays)
+struct HostBoxes {
+    const float* min_corner = nullptr; // [k][3]
+    const float* max_corner = nullptr;
+    const uint8_t* owner_kind = nullptr;
+    const uint32_t* owner_index = nullptr;
+    uint64_t k = 0;
+};
+
+UserBoxes gather_user_boxes(Ctx& c, const float* min_corner, const float* max_corner, const uint8_t* owner_kind,
+                            const uint32_t* owner_index, uint64_t k, uint64_t nv, const uint32_t* e, uint64_t ne,
+                            const uint32_t* f, uint64_t nf, bool canon, const char* what)
+{
+    cudaStream_t s = c.stream;
+    float* mn = grow<float>(c.tmp[0], 3 * k);
+    float* mx = grow<float>(c.tmp[1], 3 * k);
+    uint8_t* kd = grow<uint8_t>(c.tmp[2], k);
+    uint32_t* ix = grow<uint32_t>(c.tmp[3], k);
+    h2d(c, mn, min_corner, 12 * k);
+    h2d(c, mx, max_corner, 12 * k);
+    h2d(c, kd, owner_kind, k);
+    h2d(c, ix, owner_index, 4 * k);
+    // owner order + dense ranks
+    unsigned long long* okeys = grow<unsigned long long>(c.tmp[4], 2 * k);
+    uint32_t* pos = grow<uint32_t>(c.tmp[5], 2 * k);
+    k_owner_keys<<<grid_for(k, 256), 256, 0, s>>>(kd, ix, k, okeys, pos);
+    CCDK_LAUNCH_CHECK();
+    cub_call(c, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, okeys, okeys + k, pos, pos + k, static_cast<int64_t>(k), 0, 34,
+                                               s);
+    });
+    uint32_t* flag = grow<uint32_t>(c.tmp[6], 2 * k);
+    k_rank_flags<<<grid_for(k, 256), 256, 0, s>>>(okeys + k, k, flag);
+    cub_call(c, [&](void* t, size_t& b) {
+        return cub::DeviceScan::InclusiveSum(t, b, flag, flag + k, static_cast<int64_t>(k), s);
+    });
+    UserBoxes ub;
+    ub.bmin = grow<float>(c.bmin, 3 * k);
+    ub.bmax = grow<float>(c.bmax, 3 * k);
+    ub.vids = grow<uint4>(c.vids, k);
+    ub.raw = grow<uint32_t>(c.raw, 2 * k);
+    uint8_t* own_kind = grow<uint8_t>(c.own_kind, k);
+    uint32_t* own_index = grow<uint32_t>(c.own_index, k);
+    auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
+    CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->error, 0xff, 8, s));
+    k_gather_general<<<grid_for(k, 256), 256, 0, s>>>(mn, mx, kd, ix, pos + k, flag + k, k, nv, e, ne, f, nf,
+                                                      ub.bmin, ub.bmax, ub.vids, ub.raw, own_kind, own_index,
+                                                      &ctr->error, canon);
+    CCDK_LAUNCH_CHECK();
+    uint32_t nranks = 0;
+    unsigned long long err = 0;
+    d2h(c, &nranks, flag + 2 * k - 1, 4);
+    d2h(c, &err, &ctr->error, 8);
+    sync(c);
+    if (err != ~0ull)
+        throw Error(CCDK_INVALID_INPUT, std::string(what) + ": box owner index out of range");
+    ub.nranks = nranks;
+    return ub;
+}
+
 // run_batched's BatchRun (pipeline.cpp:81-175) over device primitives.  The
 // recursion structure, capacities and counters follow the reference so the
 // batch count and tracked bytes agree; every broad/narrow batch is a device
@@ -554,6 +633,11 @@ struct BatchRun {
     int axis = 0;
     uint64_t slabs = 0, slab_entries = 0;
     bool check_build_error = false; // the box build's flag, checked by the first broad phase
+    // a caller's box list (run_batched): raw input positions, duplicate
+    // owners, ranks = canonical slots over rank_bits
+    const uint32_t* raw = nullptr;
+    bool unique = false;
+    int rank_bits = 0;
 
     // broad_batch (pipeline.cpp:140-174): halve the sweep range while the
     // candidates exceed the budget's pair capacity
@@ -565,13 +649,19 @@ struct BatchRun {
         bi.bmax = bmax;
         bi.vids = vids;
         bi.k = k;
-        bi.method = CCDK_BROAD_STQ; // stq/sap/bf give the identical set
+        bi.raw = raw;
+        bi.unique = unique;
+        bi.rank_bits = rank_bits;
         bi.range_begin = begin;
         bi.range_end = end;
         bi.shard_rank = shard_rank;
         bi.shard_count = shard_count;
         // the axis matters only if the budget can force range halving
         bi.exact_axis = cap_pairs < k * (k - 1) / 2;
+        // stq/sap/bf give the identical set; the halved ranges differ: bf
+        // splits raw box positions, stq/sap sorted ones (pipeline.cpp:65-77)
+        bi.method = cfg.broad_method == CCDK_BROAD_BF && bi.exact_axis && shard_count == 1 ? CCDK_BROAD_BF
+                                                                                          : CCDK_BROAD_STQ;
         bi.allow_slab = allow_slab;
         bi.check_build_error = check_build_error;
         check_build_error = false; // checked at this broad phase's first read-back
@@ -747,16 +837,19 @@ struct BatchRun {
     }
 };
 
+void finish_step(Ctx& c, DevScene& s, BatchRun& run, uint64_t k, ccdk_report& rep, cudaEvent_t start_event,
+                 cudaEvent_t* ev);
+
 // The full CCD step on ctx.scene (pipeline.cpp:218-232 via run_batched at the
 // default budget): build -> STQ -> classify -> narrow -> global min.
 void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_rank, uint32_t shard_count,
-              ccdk_report& rep, cudaEvent_t start_event)
+              ccdk_report& rep, cudaEvent_t start_event, const HostBoxes* hb = nullptr)
 {
     validate_pipeline_cfg(cfg);
     std::memset(&rep, 0, sizeof rep);
     rep.toi = INFINITY;
     rep.batch_count = 1;
-    const uint64_t k = s.nv + s.ne + s.nf;
+    const uint64_t k = hb ? hb->k : s.nv + s.ne + s.nf;
     cudaStream_t st = c.stream;
     // run_batched (pipeline.cpp:184-187): candidate capacity of the budget
     const uint64_t cap_pairs = (cfg.memory_budget - cfg.rs_params) / (cfg.rs_query + 3 * cfg.rs_pair_ints);
@@ -767,6 +860,27 @@ void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_
         ev[i] = c.events.get(EventPool::kStep + i);
     CCDK_CUDA_CHECK(cudaEventRecord(ev[0], st));
 
+    if (hb) { // run_batched on the caller's boxes: no K1
+        BatchRun run { c, cfg, s, k, cap_pairs };
+        if (k) {
+            const UserBoxes ub = gather_user_boxes(c, hb->min_corner, hb->max_corner, hb->owner_kind,
+                                                   hb->owner_index, k, s.nv, s.edges.as<uint32_t>(), s.ne,
+                                                   s.faces.as<uint32_t>(), s.nf, true, "run_batched");
+            CCDK_CUDA_CHECK(cudaEventRecord(ev[1], st));
+            run.bmin = ub.bmin;
+            run.bmax = ub.bmax;
+            run.vids = ub.vids;
+            run.raw = ub.raw;
+            run.unique = ub.nranks < k;
+            run.rank_bits = ceil_log2(std::max<uint64_t>(s.nv + s.ne + s.nf, 2));
+            run.broad_batch(0, k, shard_rank, shard_count);
+        } else {
+            CCDK_CUDA_CHECK(cudaEventRecord(ev[1], st));
+            run.narrow_batches = 1;
+        }
+        finish_step(c, s, run, k, rep, start_event, ev);
+        return;
+    }
     // K1 (the scene was validated when it was uploaded)
     float* bmin = grow<float>(c.bmin, 3 * std::max<uint64_t>(k, 1));
     float* bmax = grow<float>(c.bmax, 3 * std::max<uint64_t>(k, 1));
@@ -791,6 +905,15 @@ void ccd_step(Ctx& c, DevScene& s, const ccdk_pipeline_cfg& cfg, uint32_t shard_
         run.broad_batch(0, k, shard_rank, shard_count);
     else
         run.narrow_batches = 1;
+    finish_step(c, s, run, k, rep, start_event, ev);
+}
+
+// The step's tail: the candidate union in canonical order, the export, the
+// report (pipeline.cpp:196-214).
+void finish_step(Ctx& c, DevScene& s, BatchRun& run, uint64_t k, ccdk_report& rep, cudaEvent_t start_event,
+                 cudaEvent_t* ev)
+{
+    cudaStream_t st = c.stream;
     // canonical order of the candidate union across batches (pipeline.cpp:196)
     if (run.broad_batches > 1 && run.candidates) {
         uint64_t* all = c.all_keys.as<uint64_t>();
@@ -990,6 +1113,25 @@ using namespace ccdk;
 struct ccdk_ctx : Ctx {
 };
 
+namespace {
+// An export's lifetime inside one API call: never leave with the worker
+// running or waiting.
+struct ExportScope {
+    Ctx& c;
+    ~ExportScope()
+    {
+        if (c.exp && c.exp->pending) {
+            c.exp->pending = false;
+            c.exp->aborted = true; // the worker must not deliver
+            c.exp->issued.set_value();
+        }
+        if (c.exp && c.exp->worker.joinable())
+            c.exp->worker.join();
+        c.exp = nullptr;
+    }
+};
+} // namespace
+
 extern "C" {
 
 int ccdk_abi_version(void) { return CCDK_ABI_VERSION; }
@@ -1171,53 +1313,18 @@ int ccdk_broad_phase(ccdk_ctx* ctx, int method, const float* min_corner, const f
         c.last_keys_all = false;
         if (k < 2)
             return;
-        cudaStream_t s = c.stream;
-        float* mn = grow<float>(c.tmp[0], 3 * k);
-        float* mx = grow<float>(c.tmp[1], 3 * k);
-        uint8_t* kd = grow<uint8_t>(c.tmp[2], k);
-        uint32_t* ix = grow<uint32_t>(c.tmp[3], k);
-        h2d(c, mn, min_corner, 12 * k);
-        h2d(c, mx, max_corner, 12 * k);
-        h2d(c, kd, owner_kind, k);
-        h2d(c, ix, owner_index, 4 * k);
         uint32_t* e = grow<uint32_t>(c.scene.edges, 2 * std::max<uint64_t>(ne, 1));
         uint32_t* f = grow<uint32_t>(c.scene.faces, 3 * std::max<uint64_t>(nf, 1));
         h2d(c, e, edges, 8 * ne);
         h2d(c, f, faces, 12 * nf);
         c.scene.valid = false; // only topology was uploaded
-        // owner order + dense ranks
-        unsigned long long* okeys = grow<unsigned long long>(c.tmp[4], 2 * k);
-        uint32_t* pos = grow<uint32_t>(c.tmp[5], 2 * k);
-        k_owner_keys<<<grid_for(k, 256), 256, 0, s>>>(kd, ix, k, okeys, pos);
-        CCDK_LAUNCH_CHECK();
-        cub_call(c, [&](void* t, size_t& b) {
-            return cub::DeviceRadixSort::SortPairs(t, b, okeys, okeys + k, pos, pos + k,
-                                                   static_cast<int64_t>(k), 0, 34, s);
-        });
-        uint32_t* flag = grow<uint32_t>(c.tmp[6], 2 * k);
-        k_rank_flags<<<grid_for(k, 256), 256, 0, s>>>(okeys + k, k, flag);
-        cub_call(c, [&](void* t, size_t& b) {
-            return cub::DeviceScan::InclusiveSum(t, b, flag, flag + k, static_cast<int64_t>(k), s);
-        });
-        float* bmin = grow<float>(c.bmin, 3 * k);
-        float* bmax = grow<float>(c.bmax, 3 * k);
-        uint4* vids = grow<uint4>(c.vids, k);
-        uint32_t* raw = grow<uint32_t>(c.raw, 2 * k);
-        uint8_t* own_kind = grow<uint8_t>(c.own_kind, k);
-        uint32_t* own_index = grow<uint32_t>(c.own_index, k);
-        auto* ctr = static_cast<DevCounters*>(c.counters.ensure(sizeof(DevCounters)));
-        CCDK_CUDA_CHECK(cudaMemsetAsync(&ctr->error, 0xff, 8, s));
-        k_gather_general<<<grid_for(k, 256), 256, 0, s>>>(mn, mx, kd, ix, pos + k, flag + k, k, nv, e,
-                                                          ne, f, nf, bmin, bmax, vids, raw,
-                                                          own_kind, own_index, &ctr->error);
-        CCDK_LAUNCH_CHECK();
-        uint32_t nranks = 0;
-        unsigned long long err = 0;
-        d2h(c, &nranks, flag + 2 * k - 1, 4);
-        d2h(c, &err, &ctr->error, 8);
-        sync(c);
-        if (err != ~0ull)
-            throw Error(CCDK_INVALID_INPUT, "broad phase: box owner index out of range");
+        const UserBoxes ub = gather_user_boxes(c, min_corner, max_corner, owner_kind, owner_index, k, nv, e, ne,
+                                               f, nf, false, "broad phase");
+        float* bmin = ub.bmin;
+        float* bmax = ub.bmax;
+        uint4* vids = ub.vids;
+        uint32_t* raw = ub.raw;
+        const uint64_t nranks = ub.nranks;
         BroadIn bi;
         bi.bmin = bmin;
         bi.bmax = bmax;
@@ -1690,6 +1797,7 @@ int ccdk_ccd(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv,
     });
 }
 
+
 int ccdk_ccd_into(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv, const uint32_t* edges,
                   uint64_t ne, const uint32_t* faces, uint64_t nf, const ccdk_pipeline_cfg* cfg,
                   ccdk_report* report, ccdk_pairs_sink sink, void* user)
@@ -1708,25 +1816,47 @@ int ccdk_ccd_into(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv
         PairExport x;
         x.sink = sink;
         x.user = user;
-        struct Scope { // never leave with the worker running or waiting
-            Ctx& c;
-            ~Scope()
-            {
-                if (c.exp && c.exp->pending) {
-                    c.exp->pending = false;
-                    c.exp->aborted = true; // the worker must not deliver
-                    c.exp->issued.set_value();
-                }
-                if (c.exp && c.exp->worker.joinable())
-                    c.exp->worker.join();
-                c.exp = nullptr;
-            }
-        } scope { c };
+        ExportScope scope { c };
         c.exp = &x;
         cudaEvent_t start = c.events.get(EventPool::kApi);
         CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
         upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
         ccd_step(c, c.scene, *cfg, 0, 1, *report, start);
+    });
+}
+
+int ccdk_run_batched(ccdk_ctx* ctx, const double* v0, const double* v1, uint64_t nv, const uint32_t* edges,
+                     uint64_t ne, const uint32_t* faces, uint64_t nf, const float* min_corner,
+                     const float* max_corner, const uint8_t* owner_kind, const uint32_t* owner_index, uint64_t k,
+                     const ccdk_pipeline_cfg* cfg, ccdk_report* report, ccdk_pairs_sink sink, void* user)
+{
+    return guard(ctx, [&] {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        Ctx& c = *ctx;
+        CCDK_CUDA_CHECK(cudaSetDevice(c.device));
+        validate_pipeline_cfg(*cfg);
+        if ((!v0 || !v1) && nv)
+            throw Error(CCDK_INVALID_INPUT, "vertex snapshots missing");
+        if (k && (!min_corner || !max_corner || !owner_kind || !owner_index))
+            throw Error(CCDK_INVALID_INPUT, "run_batched: box arrays missing");
+        if (k > 0xffffffffull)
+            throw Error(CCDK_INVALID_INPUT, "run_batched: more than 2^32 - 1 boxes");
+        PairExport x;
+        x.sink = sink;
+        x.user = user;
+        ExportScope scope { c };
+        if (sink)
+            c.exp = &x;
+        cudaEvent_t start = c.events.get(EventPool::kApi);
+        CCDK_CUDA_CHECK(cudaEventRecord(start, c.stream));
+        upload_scene(c, c.scene, v0, v1, nv, edges, ne, faces, nf);
+        HostBoxes hb;
+        hb.min_corner = min_corner;
+        hb.max_corner = max_corner;
+        hb.owner_kind = owner_kind;
+        hb.owner_index = owner_index;
+        hb.k = k;
+        ccd_step(c, c.scene, *cfg, 0, 1, *report, start, &hb);
     });
 }
 

@@ -1283,7 +1283,7 @@ void broad_phase(Ctx& c, const BroadIn& in, BroadOut& out)
     CCDK_LAUNCH_CHECK();
 
     // K5 sweep (re-run once with a larger buffer if the candidate count overflows)
-    const int nb = ceil_log2(k);
+    const int nb = in.rank_bits ? in.rank_bits : ceil_log2(k);
     c.last_nb = nb;
     if (c.pair_capacity < 8 * k)
         c.pair_capacity = std::max<uint64_t>(8 * k, uint64_t(1) << 20);

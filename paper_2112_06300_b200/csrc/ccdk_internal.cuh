@@ -366,6 +366,7 @@ struct BroadIn {
     uint32_t shard_rank = 0, shard_count = 1;
     bool want_rounds = false;
     bool unique = false; // duplicate owners possible
+    int rank_bits = 0;   // bits of the vids' rank space; 0 = ceil_log2(k)
     // reproduce choose_axis's serial summation order on near ties (the axis
     // is observable through choose_axis, StqStats and SweepRange slices)
     bool exact_axis = true;

@@ -139,25 +139,34 @@ std::vector<CandidatePair> fetch_pairs(uint64_t n)
     return out;
 }
 
+// A box list as the C ABI takes it: corners [k][3], owner kinds, indices.
+struct BoxArrays {
+    std::vector<float> mn, mx;
+    std::vector<uint8_t> kind;
+    std::vector<uint32_t> index;
+    explicit BoxArrays(const std::vector<Aabb>& boxes)
+        : mn(3 * boxes.size()), mx(3 * boxes.size()), kind(boxes.size()), index(boxes.size())
+    {
+        for (size_t i = 0; i < boxes.size(); ++i) {
+            for (int c = 0; c < 3; ++c) {
+                mn[3 * i + c] = boxes[i].min_corner[c];
+                mx[3 * i + c] = boxes[i].max_corner[c];
+            }
+            kind[i] = uint8_t(boxes[i].owner.kind);
+            index[i] = boxes[i].owner.index;
+        }
+    }
+};
+
 std::vector<CandidatePair> broad(int method, const std::vector<Aabb>& boxes, const SceneStep& scene,
                                  StqStats* stats, SweepRange range)
 {
     SequenceGuard g(sequence_mutex());
     const size_t k = boxes.size();
-    std::vector<float> mn(3 * k), mx(3 * k);
-    std::vector<uint8_t> kind(k);
-    std::vector<uint32_t> index(k);
-    for (size_t i = 0; i < k; ++i) {
-        for (int c = 0; c < 3; ++c) {
-            mn[3 * i + c] = boxes[i].min_corner[c];
-            mx[3 * i + c] = boxes[i].max_corner[c];
-        }
-        kind[i] = uint8_t(boxes[i].owner.kind);
-        index[i] = boxes[i].owner.index;
-    }
+    const BoxArrays b(boxes);
     uint64_t n = 0;
     ccdk_stq_stats st {};
-    check(ccdk_broad_phase(context(), method, mn.data(), mx.data(), kind.data(), index.data(), k,
+    check(ccdk_broad_phase(context(), method, b.mn.data(), b.mx.data(), b.kind.data(), b.index.data(), k,
                            scene.vertices_t0.size(), edata(scene), scene.edges.size(), fdata(scene),
                            scene.faces.size(), range.begin, range.end, &n, stats ? &st : nullptr));
     std::vector<CandidatePair> out = fetch_pairs(n);
@@ -578,32 +587,36 @@ CCDKIT_EXPORT ToiResult run_batched(const SceneStep& scene, const std::vector<Aa
                                     const PipelineConfig& cfg, BatchTrace& trace, CcdReport* report)
 {
     cfg.validate();
-    // the device step rebuilds the boxes; they must be this scene's own
-    const std::vector<Aabb> own = build_boxes(scene, cfg.inflation);
-    bool same = own.size() == boxes.size();
-    for (size_t i = 0; same && i < own.size(); ++i)
-        same = own[i].min_corner == boxes[i].min_corner && own[i].max_corner == boxes[i].max_corner
-            && own[i].owner == boxes[i].owner;
-    if (!same)
-        throw ConfigError("run_batched: boxes must equal build_boxes(scene, cfg.inflation)");
+    if (scene.vertices_t0.size() != scene.vertices_t1.size()) // element checks: on the device
+        throw InvalidInput("vertex snapshots differ in length");
+    // the caller's boxes, any order, through the device broad phase
+    // (ccdk_run_batched: batches halve sorted positions, raw ones for bf)
+    const BoxArrays b(boxes);
     const ccdk_pipeline_cfg c = to_c(cfg);
     ccdk_report r {};
+    std::vector<CandidatePair> cands;
+    CandidateSink sink { &cands, nullptr };
     SequenceGuard g(sequence_mutex());
-    check(ccdk_ccd(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1), scene.vertices_t0.size(),
-                   edata(scene), scene.edges.size(), fdata(scene), scene.faces.size(), &c, &r));
+    const int rc = ccdk_run_batched(context(), vdata(scene.vertices_t0), vdata(scene.vertices_t1),
+                                    scene.vertices_t0.size(), edata(scene), scene.edges.size(), fdata(scene),
+                                    scene.faces.size(), b.mn.data(), b.mx.data(), b.kind.data(), b.index.data(),
+                                    boxes.size(), &c, &r, report ? candidate_sink : nullptr, &sink);
+    if (sink.err)
+        std::rethrow_exception(sink.err);
+    check(rc);
     trace.broad_batches += r.broad_batches;
     trace.narrow_batches += r.batch_count;
     if (report) { // exactly the fields the reference's run_batched writes (pipeline.cpp:198-214)
-        CcdReport fresh = to_report(r, true);
+        const CcdReport fresh = to_report(r, false);
         report->toi = fresh.toi;
         report->candidate_count = fresh.candidate_count;
         report->query_count = fresh.query_count;
-        report->batch_count = fresh.batch_count;
-        report->per_stage_times["BP"] = fresh.per_stage_times["BP"];
-        report->per_stage_times["SO/CD"] = fresh.per_stage_times["SO/CD"];
-        report->per_stage_times["NP"] = fresh.per_stage_times["NP"];
+        report->batch_count = std::max<std::size_t>(1, trace.narrow_batches);
+        report->per_stage_times["BP"] = r.t_bp;
+        report->per_stage_times["SO/CD"] = r.t_socd;
+        report->per_stage_times["NP"] = r.t_np;
         report->tracked_peak_bytes = std::max(report->tracked_peak_bytes, fresh.tracked_peak_bytes);
-        report->candidates = std::move(fresh.candidates);
+        report->candidates = std::move(cands);
         report->real_record_sizes = fresh.real_record_sizes;
     }
     return { r.toi, r.tolerance_hit != 0, r.zero_toi_diagnostic != 0 };

@@ -79,6 +79,10 @@ _SIGS = {
                                 C.c_uint64, C.POINTER(abi.PipelineCfg), C.POINTER(abi.Report),
                                 C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64),
                                 C.c_void_p]),
+    "ccdk_run_batched": (C.c_int, [C.c_void_p, P_F64, P_F64, C.c_uint64, P_U32, C.c_uint64, P_U32,
+                                   C.c_uint64, P_F32, P_F32, P_U8, P_U32, C.c_uint64,
+                                   C.POINTER(abi.PipelineCfg), C.POINTER(abi.Report), C.c_void_p,
+                                   C.c_void_p]),  # sink: a ccdk_pairs_sink or None
     "ccdk_ccd_no_zero_toi": (C.c_int, [C.c_void_p, P_F64, P_F64, C.c_uint64, P_U32, C.c_uint64, P_U32,
                                        C.c_uint64, C.POINTER(abi.PipelineCfg), C.POINTER(abi.Report)]),
     "ccdk_query_min_separations": (C.c_int, [C.c_void_p, P_U8, P_F64, C.c_uint64,

@@ -2,6 +2,7 @@
 // libccdkit.so -> libccdk.so).  Re-authored from the reference's doctest
 // suites (proj/tests/test_{geometry,broadphase,narrowphase,pipeline}.cpp) with
 // a minimal harness; built and run by tests/test_cpp_api.py on the GPU box.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <exception>
@@ -232,6 +233,54 @@ static void determinism_across_threads()
         CHECK(bad[t] == 0);
 }
 
+// run_batched on a caller's box list (pipeline.cpp:179-215): reversed order,
+// padded boxes and a duplicated owner sweep like any other list; the report
+// keeps the fields run_batched does not write (CB); the trace accumulates.
+static void run_batched_on_a_box_list()
+{
+    const SceneStep s = grid_scene(10, 0.01);
+    std::vector<Aabb> boxes = build_boxes(s, 0.0);
+    std::reverse(boxes.begin(), boxes.end());
+    for (Aabb& b : boxes)
+        for (int c = 0; c < 3; ++c) {
+            b.min_corner[c] -= 0.05f;
+            b.max_corner[c] += 0.05f;
+        }
+    boxes.push_back(boxes.front());
+    // the expected list: the broad phase on the same boxes + classify/narrow
+    const auto pairs = stq(boxes, s);
+    const ClassifiedQueries q = classify(pairs, s);
+    std::vector<NarrowQuery> all = q.vertex_face;
+    all.insert(all.end(), q.edge_edge.begin(), q.edge_edge.end());
+    const NarrowOutcome o = narrow_phase(all, NarrowConfig {});
+    BatchTrace trace;
+    CcdReport rep;
+    rep.per_stage_times["CB"] = 0.25;
+    const ToiResult t = run_batched(s, boxes, PipelineConfig {}, trace, &rep);
+    CHECK(rep.candidates == pairs);
+    CHECK(t.toi == o.global_toi && rep.toi.toi == t.toi);
+    CHECK(rep.query_count == all.size() && trace.broad_batches == 1 && trace.narrow_batches == 1);
+    CHECK(rep.per_stage_times["CB"] == 0.25);
+    // a small budget: several broad batches.  Each batch is deduplicated on
+    // its own and the union is only sorted (pipeline.cpp:196), so the
+    // duplicated owner can repeat a pair across batches, as in the reference
+    PipelineConfig small;
+    small.memory_budget = 1 << 15;
+    CcdReport rs;
+    const ToiResult ts = run_batched(s, boxes, small, trace, &rs);
+    std::vector<CandidatePair> uniq = rs.candidates;
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    CHECK(ts.toi == t.toi && uniq == pairs && std::is_sorted(rs.candidates.begin(), rs.candidates.end()));
+    CHECK(trace.broad_batches > 2);
+    CHECK(rs.batch_count == trace.narrow_batches);
+    std::printf("run_batched: %zu candidates, budget 2^15: trace %zu broad / %zu narrow batches\n", pairs.size(),
+                trace.broad_batches, trace.narrow_batches);
+    // owners must name existing primitives
+    std::vector<Aabb> bad = boxes;
+    bad[0].owner.index = 1u << 30;
+    CHECK_THROWS_AS(run_batched(s, bad, PipelineConfig {}, trace, nullptr), InvalidInput);
+}
+
 int main()
 {
     try {
@@ -240,6 +289,7 @@ int main()
         narrowphase();
         pipeline();
         determinism_across_threads();
+        run_batched_on_a_box_list();
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         return 2;
