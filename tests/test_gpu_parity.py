@@ -383,12 +383,15 @@ def test_query_min_separations_bit_exact(ctx, ref):
 
 
 def test_relative_min_sep_pipeline(ctx, ref):
-    s = scenes.make_box_soup(40, 5.0, 0.4, 1.0, 1005)
+    # a colliding soup small enough for the reference: its narrow phase is
+    # slow on relative-mode contacts (a 40-body soup took 3 min on 16 cores)
+    s = scenes.make_box_soup(6, 3.0, 0.4, 1.0, 2)
     cfg = PipelineConfig(min_sep_mode=ck.MINSEP_RELATIVE, inflation=0.01)
     got = ck.ccd(s, cfg, ctx=ctx)
     exp, pairs = ref.ccd(s, cfg.to_c())
     assert got.toi.toi == exp.toi and got.toi.tolerance_hit == bool(exp.tolerance_hit)
     np.testing.assert_array_equal(got.candidates, pairs)
+    assert exp.toi < 1.0  # the relative separations decide a real contact
 
 
 def test_zero_toi_retry(ctx, ref):
