@@ -132,3 +132,23 @@ def test_ccd_restatement(ref, orc):
         np.testing.assert_array_equal(pa, pb)
         assert ra.toi == rb.toi and ra.candidate_count == rb.candidate_count
         assert ra.query_count == rb.query_count and ra.tolerance_hit == rb.tolerance_hit
+
+
+def test_ref_run_batched_adapter(ref, orc):
+    """The adapter's run_batched (the GPU tests' reference for ccdk_run_batched)
+    on the scene's own boxes reproduces ccd (pipeline.cpp:218-232 is exactly
+    build_boxes + run_batched); with a small budget the union is the same set
+    and the trace counts the batches that ran."""
+    s = scenes.make_cloth_scene(20, 20, 0.02, 1.0, 1)
+    cfg = abi.pipeline_cfg(inflation=0.01)
+    boxes = orc.build_boxes(s, 0.01)
+    ra, pa = ref.ccd(s, cfg)
+    rb, pb, bb, nb = ref.run_batched(s, boxes, cfg)
+    np.testing.assert_array_equal(pa, pb)
+    assert (ra.toi, ra.candidate_count, ra.query_count, ra.batch_count) == \
+        (rb.toi, rb.candidate_count, rb.query_count, rb.batch_count)
+    assert (bb, nb) == (1, 1) and rb.tracked_peak_bytes == ra.tracked_peak_bytes
+    small = abi.pipeline_cfg(inflation=0.01, memory_budget=1 << 19)
+    rc, pc, bb, nb = ref.run_batched(s, boxes, small)
+    np.testing.assert_array_equal(pc, pa)
+    assert rc.toi == ra.toi and bb > 1 and nb >= bb and rc.batch_count == nb
