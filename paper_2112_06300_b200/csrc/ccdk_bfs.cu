@@ -1258,6 +1258,13 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
         c.gen_acc.resize(ng, 0);
     for (uint64_t g = 0; g < ng; ++g)
         c.gen_acc[g] += host_gs[g];
+    static const bool gen_trace = std::getenv("CCDK_GEN_TRACE") != nullptr;
+    if (gen_trace) { // diagnostics: intervals per generation of this run
+        fprintf(stderr, "[ccdk gens] n=%llu", (unsigned long long)n);
+        for (uint64_t g = 0; g < ng; ++g)
+            fprintf(stderr, " %llu", (unsigned long long)host_gs[g]);
+        fprintf(stderr, "\n");
+    }
     st.total_splits += host_sc->total_splits;
     st.evaluations += host_sc->evaluations;
     st.split_actions += host_sc->split_actions;
