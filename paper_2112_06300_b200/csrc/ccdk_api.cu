@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <emmintrin.h>
 #include <memory>
 #include <thread>
 
@@ -370,10 +371,13 @@ void check_scene_error(Ctx& c)
 // Host -> device copies of a scene's arrays.  Pinned sources go straight to
 // the DMA engine.  Pageable sources (ordinary std::vector storage, the
 // drop-in's case) are copied by the host into the context's pinned staging
-// buffer in 2 MB chunks, several threads at once for large scenes, and each
+// buffer in 1 MB chunks, several threads at once for large scenes, and each
 // chunk's DMA is enqueued as soon as it is staged — the host copy and the
 // transfer overlap instead of the driver's serial pageable path (measured
-// ~10 GB/s for a 16 MB scene).
+// ~10 GB/s for a 16 MB scene).  The staging stores are non-temporal: with
+// ordinary stores the host's memory bandwidth, shared by the copy's reads,
+// writes and read-for-ownership and the DMA's reads, held the 16 MB C4
+// upload at 1.1 ms; streaming stores take it to 0.5 ms (tools/upload_sweep.sh).
 struct HostPiece {
     void* dst;
     const void* src;
@@ -390,9 +394,43 @@ bool is_pinned(const void* p)
     return at.type == cudaMemoryTypeHost;
 }
 
+// Copy into pinned staging with non-temporal stores: the staging lines are
+// read next by the DMA engine, not the CPU, so skipping the read-for-ownership
+// saves a third of the host memory traffic of the copy (dst 16-byte aligned).
+void stream_copy(void* dst, const void* src, size_t n)
+{
+    auto* d = static_cast<__m128i*>(dst);
+    const auto* s = static_cast<const __m128i*>(src);
+    const size_t v = n / 16;
+    for (size_t i = 0; i < v; i += 4) {
+        if (i + 4 <= v) {
+            const __m128i a = _mm_loadu_si128(s + i), b = _mm_loadu_si128(s + i + 1);
+            const __m128i e = _mm_loadu_si128(s + i + 2), f = _mm_loadu_si128(s + i + 3);
+            _mm_stream_si128(d + i, a);
+            _mm_stream_si128(d + i + 1, b);
+            _mm_stream_si128(d + i + 2, e);
+            _mm_stream_si128(d + i + 3, f);
+        } else {
+            for (size_t j = i; j < v; ++j)
+                _mm_stream_si128(d + j, _mm_loadu_si128(s + j));
+        }
+    }
+    std::memcpy(static_cast<char*>(dst) + 16 * v, static_cast<const char*>(src) + 16 * v, n - 16 * v);
+    _mm_sfence();
+}
+
+size_t env_size(const char* name, size_t dflt)
+{
+    const char* v = std::getenv(name);
+    return v && *v ? static_cast<size_t>(std::strtoull(v, nullptr, 10)) : dflt;
+}
+
 void upload_pieces(Ctx& c, const HostPiece* pieces, int n)
 {
-    constexpr size_t kChunk = size_t(2) << 20;
+    // staging chunk and helper count (CCDK_STAGE_CHUNK_KB / CCDK_STAGE_THREADS: A/B switches)
+    static const size_t kChunk = env_size("CCDK_STAGE_CHUNK_KB", 1024) << 10;
+    static const size_t kMaxHelpers = env_size("CCDK_STAGE_THREADS", 7);
+    static const bool kStream = env_size("CCDK_STAGE_NT", 1) != 0;
     size_t staged = 0;
     struct Chunk {
         void* dst;
@@ -423,18 +461,51 @@ void upload_pieces(Ctx& c, const HostPiece* pieces, int n)
     std::atomic<size_t> next { 0 };
     std::atomic<int> failed { 0 };
     const int device = c.device;
+    static const bool trace = std::getenv("CCDK_UPLOAD_TRACE") != nullptr;
+    using TClock = std::chrono::steady_clock;
+    const auto t0 = TClock::now();
+    std::vector<double> tr(trace ? 3 * chunks.size() : 0);
+    auto us = [&] { return std::chrono::duration<double, std::micro>(TClock::now() - t0).count(); };
     auto work = [&, device] {
         cudaSetDevice(device); // helper threads start on device 0
         for (size_t k; (k = next.fetch_add(1)) < chunks.size();) {
             const Chunk& ch = chunks[k];
-            std::memcpy(pin + ch.off, ch.src, ch.bytes);
+            if (trace)
+                tr[3 * k] = us();
+            if (kStream)
+                stream_copy(pin + ch.off, ch.src, ch.bytes);
+            else
+                std::memcpy(pin + ch.off, ch.src, ch.bytes);
+            if (trace)
+                tr[3 * k + 1] = us();
             if (cudaMemcpyAsync(ch.dst, pin + ch.off, ch.bytes, cudaMemcpyHostToDevice, c.stream) != cudaSuccess)
                 failed = 1;
+            if (trace)
+                tr[3 * k + 2] = us();
         }
     };
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned helpers = static_cast<unsigned>(std::min<size_t>({ 7, hw / 2, chunks.size() / 2 }));
+    const unsigned helpers = static_cast<unsigned>(std::min<size_t>({ kMaxHelpers, hw / 2, chunks.size() / 2 }));
+    cudaEvent_t ev[2] = { nullptr, nullptr };
+    if (trace) {
+        cudaEventCreate(&ev[0]);
+        cudaEventCreate(&ev[1]);
+        cudaEventRecord(ev[0], c.stream);
+    }
     c.host_pool.run(work, helpers);
+    if (trace) { // diagnostics: per chunk (copy start, copy end, DMA enqueued) in us
+        cudaEventRecord(ev[1], c.stream);
+        cudaEventSynchronize(ev[1]);
+        float gms = 0;
+        cudaEventElapsedTime(&gms, ev[0], ev[1]);
+        fprintf(stderr, "[ccdk upload] stream %.0f us, host sync at %.0f us; ", 1000 * gms, us());
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        fprintf(stderr, "%zu chunks, %u helpers:", chunks.size(), helpers);
+        for (size_t k = 0; k < chunks.size(); ++k)
+            fprintf(stderr, " (%.0f %.0f %.0f)", tr[3 * k], tr[3 * k + 1], tr[3 * k + 2]);
+        fprintf(stderr, " returned %.0f\n", us());
+    }
     if (failed)
         CCDK_CUDA_CHECK(cudaGetLastError());
 }
@@ -453,9 +524,18 @@ void upload_scene(Ctx& c, DevScene& s, const double* v0, const double* v1, uint6
                                   { s.v1.ensure(nv * 24), v1, nv * 24 },
                                   { s.edges.ensure(ne * 8), e, ne * 8 },
                                   { s.faces.ensure(nf * 12), f, nf * 12 } };
+    static const bool trace = std::getenv("CCDK_UPLOAD_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     upload_pieces(c, pieces, 4);
+    if (trace)
+        sync(c);
+    const auto t1 = std::chrono::steady_clock::now();
     validate_scene_dev(c, s);
     check_scene_error(c);
+    if (trace) // diagnostics: exposed upload and validation time
+        fprintf(stderr, "[ccdk upload] %.3f ms copies, %.3f ms validation\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
     s.valid = true;
 }
 
