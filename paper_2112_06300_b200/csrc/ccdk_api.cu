@@ -399,6 +399,10 @@ bool is_pinned(const void* p)
 // saves a third of the host memory traffic of the copy (dst 16-byte aligned).
 void stream_copy(void* dst, const void* src, size_t n)
 {
+    if (reinterpret_cast<uintptr_t>(dst) & 15) {
+        std::memcpy(dst, src, n);
+        return;
+    }
     auto* d = static_cast<__m128i*>(dst);
     const auto* s = static_cast<const __m128i*>(src);
     const size_t v = n / 16;
@@ -449,7 +453,7 @@ void upload_pieces(Ctx& c, const HostPiece* pieces, int n)
         for (size_t o = 0; o < pc.bytes; o += kChunk) {
             const size_t b = std::min(kChunk, pc.bytes - o);
             chunks.push_back({ static_cast<char*>(pc.dst) + o, static_cast<const char*>(pc.src) + o, b, staged });
-            staged += b;
+            staged += (b + 63) & ~size_t(63); // staging slots 64-byte aligned (streaming stores)
         }
     }
     if (chunks.empty())

@@ -93,10 +93,35 @@ __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned v)
         atomicAdd(dst, static_cast<unsigned long long>(s));
 }
 
+// L2 eviction priority of the generation's loads (CCDK_REC_POLICY, A/B
+// switch): 1 = query records evict_last (re-read by the query's next
+// intervals one generation later), 2 = plus the interval records of the
+// current generation evict_first (dead after this read).
+#ifndef CCDK_REC_POLICY
+#define CCDK_REC_POLICY 2
+#endif
+__device__ __forceinline__ unsigned long long policy_evict_last()
+{
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_first()
+{
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
 {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8_hint(void* smem, const void* gmem, unsigned long long pol)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
+                 : "memory");
 }
 // 16-byte copies through L1 (.ca) or L2 only (.cg)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool l1)
@@ -106,6 +131,16 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool l1
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
     else
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, bool l1, unsigned long long pol)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if (l1)
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
+                     : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
+                     : "memory");
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 {
@@ -320,6 +355,12 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     if (b >= nbatch)
         return; // warp-uniform; no __syncthreads in this kernel
 
+#if CCDK_REC_POLICY >= 1
+    const unsigned long long pol_keep = policy_evict_last();
+#endif
+#if CCDK_REC_POLICY >= 2
+    const unsigned long long pol_dead = policy_evict_first();
+#endif
     auto issue = [&](unsigned long long bb, unsigned q, int st) {
         // batch bb's coordinates + record + query scalars, batch bb+W's ids
         if (bb < nbatch) {
@@ -344,13 +385,26 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                 // the record's 12 (x0, x1) pairs (internal order), pair-major
                 double* coords = stage0 + st * kStageDoubles;
                 const double* src = a.pts + 24ull * q;
+#if CCDK_REC_POLICY >= 1
+#pragma unroll
+                for (int k = 0; k < 12; ++k)
+                    cp_async16_hint(coords + 64 * k + 2 * lane, src + 2 * k, l1_records, pol_keep);
+#else
 #pragma unroll
                 for (int k = 0; k < 12; ++k)
                     cp_async16(coords + 64 * k + 2 * lane, src + 2 * k, l1_records);
+#endif
+#if CCDK_REC_POLICY >= 2
+                cp_async8_hint(meta + 32 * kMT + lane, R.t + i, pol_dead);
+                cp_async8_hint(meta + 32 * kMU + lane, R.u + i, pol_dead);
+                cp_async8_hint(meta + 32 * kMV + lane, R.v + i, pol_dead);
+                cp_async8_hint(meta + 32 * kMDep + lane, R.dep + i, pol_dead);
+#else
                 cp_async8(meta + 32 * kMT + lane, R.t + i);
                 cp_async8(meta + 32 * kMU + lane, R.u + i);
                 cp_async8(meta + 32 * kMV + lane, R.v + i);
                 cp_async8(meta + 32 * kMDep + lane, R.dep + i);
+#endif
                 cp_async8(meta + 32 * kMSnap + lane, a.snap + q);
                 unsigned* ex = reinterpret_cast<unsigned*>(meta + 32 * kMExh + lane);
                 cp_async4(ex, a.exh_gen + q);
