@@ -350,6 +350,9 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 // reference, and in the Fast path (no NaN) min/max are order-independent.
 // Samples: dim D holds (lo, mid, hi), the others (lo, hi); child 0 takes
 // indices {0, 1} along D, child 1 {1, 2}.
+#ifndef CCDK_UNIFIED_SU
+#define CCDK_UNIFIED_SU 1
+#endif
 struct PairBox {
     double t[3], u[3], v[3];
 };
@@ -379,6 +382,24 @@ __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const Pair
             const I s = scale<W>(t, dl[p]);
             at[p] = { W::dn(__dadd_rn(x0[p], s.lo)), W::up(__dadd_rn(x0[p], s.hi)) };
         }
+#if CCDK_UNIFIED_SU
+        // One formula for both kinds (no per-lane select between add and
+        // sub: predication issued both).  EE's base + u (p1 - p0) is formed
+        // as base - u (p0 - p1): Fast widening is sign-symmetric
+        // (dn(-x) = -up(x)) and negation is exact, so sub(p0, p1) is exactly
+        // the negated sub(p1, p0), scale(u >= 0, .) commutes with it, and
+        // sub(base, -w) is bit for bit add(base, w) (x - (-y) == x + y in
+        // IEEE arithmetic, zeros included; the Fast path never sees a NaN).
+        const I a_org = vf ? at[1] : at[2];
+        const I a_uto = vf ? at[2] : at[0];
+        const I base = sub<W>(at[0], a_org);
+        const I du = sub<W>(a_uto, at[1]);
+        const I dv = sub<W>(at[3], a_org);
+        I su[NU], vt[NV];
+#pragma unroll
+        for (int iu = 0; iu < NU; ++iu)
+            su[iu] = sub<W>(base, scale<W>(b.u[iu], du));
+#else
         const I a_org = vf ? at[1] : at[2];
         const I a_uto = vf ? at[2] : at[1];
         const I a_ufr = vf ? at[1] : at[0];
@@ -391,6 +412,7 @@ __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const Pair
             const I ut = scale<W>(b.u[iu], du);
             su[iu] = vf ? sub<W>(base, ut) : add<W>(base, ut);
         }
+#endif
 #pragma unroll
         for (int iv = 0; iv < NV; ++iv)
             vt[iv] = scale<W>(b.v[iv], dv);
