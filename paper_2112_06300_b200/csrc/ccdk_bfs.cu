@@ -40,6 +40,9 @@ constexpr int kGenUnroll = CCDK_GEN_UNROLL; // generations per WHILE iteration o
 #define CCDK_PDL 1
 #endif
 constexpr bool kUsePdl = CCDK_PDL != 0; // programmatic dependent launch inside the generation chain
+#ifndef CCDK_DEFER_APPEND
+#define CCDK_DEFER_APPEND 0
+#endif
 #ifndef CCDK_GEN_MINB
 #define CCDK_GEN_MINB 3
 #endif
@@ -197,6 +200,55 @@ __device__ __forceinline__ void append_splits(const GenArgs& a, int nb, unsigned
     unsigned long long base = 0;
     if (my_cnt)
         base = atomicAdd(&a.sc->next_pairs[lane], static_cast<unsigned long long>(my_cnt));
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+        const int d = r[ch].dim;
+        const unsigned long long b = __shfl_sync(0xffffffffu, base, d < 0 ? 0 : d);
+        if (d < 0)
+            continue;
+        const unsigned long long slot = b + off[ch];
+        const Region& R = a.reg[nb][d];
+        if (slot < a.cap_pairs) {
+            R.qid[slot] = q;
+            R.t[slot] = r[ch].tlo;
+            R.u[slot] = r[ch].ulo;
+            R.v[slot] = r[ch].vlo;
+            R.dep[slot] = r[ch].dp;
+        } else {
+            a.sc->phys_overflow = 1;
+        }
+    }
+}
+
+// The same append in two halves (CCDK_DEFER_APPEND): the cursor atomic is
+// issued at the end of a batch and its result consumed only after the next
+// batch's loads are issued, so the atomic's round trip overlaps the loop
+// head instead of stalling the shuffle right behind it.
+__device__ __forceinline__ void append_reserve(const GenArgs& a, unsigned lane, const SplitRec r[2], unsigned off[2],
+                                               unsigned long long& base)
+{
+    const unsigned lt = (1u << lane) - 1;
+    off[0] = off[1] = 0;
+    unsigned my_cnt = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const unsigned m0 = __ballot_sync(0xffffffffu, r[0].dim == d);
+        const unsigned m1 = __ballot_sync(0xffffffffu, r[1].dim == d);
+        if (r[0].dim == d)
+            off[0] = __popc(m0 & lt);
+        if (r[1].dim == d)
+            off[1] = __popc(m0) + __popc(m1 & lt);
+        if (lane == static_cast<unsigned>(d))
+            my_cnt = __popc(m0) + __popc(m1);
+    }
+    base = 0;
+    if (my_cnt)
+        base = atomicAdd(&a.sc->next_pairs[lane], static_cast<unsigned long long>(my_cnt));
+}
+
+__device__ __forceinline__ void append_write(const GenArgs& a, int nb, unsigned q, const SplitRec r[2],
+                                             const unsigned off[2], unsigned long long base)
+{
 #pragma unroll
     for (int ch = 0; ch < 2; ++ch) {
         const int d = r[ch].dim;
@@ -432,6 +484,13 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
     }
     issue(b, q_cur, 0);
     int st = 0;
+#if CCDK_DEFER_APPEND
+    SplitRec pr[2]; // split records of the previous batch, appended after the next issue
+    pr[0].dim = pr[1].dim = -1;
+    unsigned poff[2] = { 0, 0 };
+    unsigned long long pbase = 0;
+    unsigned pq = 0;
+#endif
 
     for (; b < nbatch; b += W) {
         cp_async_wait<0>(); // batch b's data and batch b+W's ids (issued one batch ago)
@@ -450,6 +509,9 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
         q_cur = qbuf[lane];
         // batch b+W streams into the other coordinate buffer while b is evaluated
         issue(b + W, q_cur, st ^ 1);
+#if CCDK_DEFER_APPEND
+        append_write(a, nb, pq, pr, poff, pbase); // the previous batch's split records
+#endif
 
         SplitRec r[2];
         r[0].dim = r[1].dim = -1;
@@ -561,9 +623,19 @@ __global__ void __launch_bounds__(kGenBlock, CCDK_GEN_MINB) k_generation(GenArgs
                     a.exh_gen[q] = gen;
             }
         }
+#if CCDK_DEFER_APPEND
+        append_reserve(a, lane, r, poff, pbase);
+        pr[0] = r[0];
+        pr[1] = r[1];
+        pq = q;
+#else
         append_splits(a, nb, lane, q, r);
+#endif
         st ^= 1;
     }
+#if CCDK_DEFER_APPEND
+    append_write(a, nb, pq, pr, poff, pbase);
+#endif
     cp_async_wait<0>();
     warp_add(&sc->evaluations, evals);
     warp_add(&sc->split_actions, split_actions);

@@ -23,6 +23,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace ccdk {
 namespace iv {
@@ -196,17 +197,27 @@ __device__ __forceinline__ void component(bool vf, const Pts& P, const Box& b, i
                 at[p] = { W::dn(__dadd_rn(x0[p], s.lo)), W::up(__dadd_rn(x0[p], s.hi)) };
             }
             // VF: origin 1, u 1->2; EE: origin 2, u 0->1 (selects, not runtime indexing)
-            const I a_org = vf ? at[1] : at[2];
-            const I a_uto = vf ? at[2] : at[1];
-            const I a_ufr = vf ? at[1] : at[0];
-            const I base = sub<W>(at[0], a_org);
-            const I du = sub<W>(a_uto, a_ufr);
-            const I dv = sub<W>(at[3], a_org);
             I su[2], vt[2];
+            const I a_org = vf ? at[1] : at[2];
+            const I base = sub<W>(at[0], a_org);
+            const I dv = sub<W>(at[3], a_org);
+            if constexpr (std::is_same_v<W, Fast>) {
+                // one formula for both kinds, as in component_pair (below)
+                const I du = sub<W>(vf ? at[2] : at[0], at[1]);
 #pragma unroll
-            for (int cu = 0; cu < 2; ++cu) {
-                const I ut = scale<W>(cu ? b.uhi : b.ulo, du);
-                su[cu] = vf ? sub<W>(base, ut) : add<W>(base, ut);
+                for (int cu = 0; cu < 2; ++cu)
+                    su[cu] = sub<W>(base, scale<W>(cu ? b.uhi : b.ulo, du));
+            } else {
+                // Exact widening: NaN operands are possible, keep the
+                // reference's add for EE (a negated NaN changes sign bits)
+                const I a_uto = vf ? at[2] : at[1];
+                const I a_ufr = vf ? at[1] : at[0];
+                const I du = sub<W>(a_uto, a_ufr);
+#pragma unroll
+                for (int cu = 0; cu < 2; ++cu) {
+                    const I ut = scale<W>(cu ? b.uhi : b.ulo, du);
+                    su[cu] = vf ? sub<W>(base, ut) : add<W>(base, ut);
+                }
             }
 #pragma unroll
             for (int cv = 0; cv < 2; ++cv)
