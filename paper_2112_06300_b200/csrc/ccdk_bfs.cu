@@ -220,6 +220,7 @@ __device__ __forceinline__ void append_splits(const GenArgs& a, int nb, unsigned
     }
 }
 
+#if CCDK_DEFER_APPEND
 // The same append in two halves (CCDK_DEFER_APPEND): the cursor atomic is
 // issued at the end of a batch and its result consumed only after the next
 // batch's loads are issued, so the atomic's round trip overlaps the loop
@@ -268,6 +269,7 @@ __device__ __forceinline__ void append_write(const GenArgs& a, int nb, unsigned 
         }
     }
 }
+#endif
 
 // ---- generation 0: the roots [0,1]^3, one thread per query, coordinates
 // read straight from the query record (one generation of the ~80).

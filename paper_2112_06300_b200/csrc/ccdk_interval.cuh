@@ -361,6 +361,9 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 // reference, and in the Fast path (no NaN) min/max are order-independent.
 // Samples: dim D holds (lo, mid, hi), the others (lo, hi); child 0 takes
 // indices {0, 1} along D, child 1 {1, 2}.
+#ifndef CCDK_SLICE_HULL
+#define CCDK_SLICE_HULL 1
+#endif
 #ifndef CCDK_UNIFIED_SU
 #define CCDK_UNIFIED_SU 1
 #endif
@@ -428,6 +431,60 @@ __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const Pair
         for (int iv = 0; iv < NV; ++iv)
             vt[iv] = scale<W>(b.v[iv], dv);
         double m[NU * NV];
+#if CCDK_SLICE_HULL
+        // Hulls through slices: the corners of one sample along D form a
+        // slice whose hull is folded once and shared by both children (the
+        // midpoint slice belongs to both).  min/max over a child's corners
+        // is order-independent here (Fast path: no NaN; widened bounds are
+        // never +/-0), so the grouping is bit-identical to the corner fold.
+        auto corner = [&](int iu, int iv) -> I {
+            const I f = sub<W>(su[iu], vt[iv]);
+            m[iu * NV + iv] = mid2(f);
+            return f;
+        };
+        auto hull = [](I& acc, const I& f) {
+            acc.lo = smin(acc.lo, f.lo);
+            acc.hi = smax(acc.hi, f.hi);
+        };
+        if constexpr (D == 0) {
+            I sl = corner(0, 0);
+            hull(sl, corner(0, 1));
+            hull(sl, corner(1, 0));
+            hull(sl, corner(1, 1));
+            if (it == 0) {
+                rng[0] = sl;
+            } else if (it == 1) {
+                hull(rng[0], sl);
+                rng[1] = sl;
+            } else {
+                hull(rng[1], sl);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) { // sample index along D
+                I sl;
+                if constexpr (D == 1) {
+                    sl = corner(k, 0);
+                    hull(sl, corner(k, 1));
+                } else {
+                    sl = corner(0, k);
+                    hull(sl, corner(1, k));
+                }
+                if (k <= 1) {
+                    if (it == 0 && k == 0)
+                        rng[0] = sl;
+                    else
+                        hull(rng[0], sl);
+                }
+                if (k >= 1) {
+                    if (it == 0 && k == 1)
+                        rng[1] = sl;
+                    else
+                        hull(rng[1], sl);
+                }
+            }
+        }
+#else
 #pragma unroll
         for (int iu = 0; iu < NU; ++iu) {
 #pragma unroll
@@ -450,6 +507,7 @@ __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const Pair
                 }
             }
         }
+#endif
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
             if (D == 0 && !(it == ch || it == ch + 1))
