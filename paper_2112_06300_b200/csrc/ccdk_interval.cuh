@@ -361,6 +361,9 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 // reference, and in the Fast path (no NaN) min/max are order-independent.
 // Samples: dim D holds (lo, mid, hi), the others (lo, hi); child 0 takes
 // indices {0, 1} along D, child 1 {1, 2}.
+#ifndef CCDK_TWICE_MID
+#define CCDK_TWICE_MID 0
+#endif
 #ifndef CCDK_SLICE_HULL
 #define CCDK_SLICE_HULL 1
 #endif
@@ -370,6 +373,22 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 struct PairBox {
     double t[3], u[3], v[3];
 };
+
+// Corner "midpoints" for the influences.  With CCDK_TWICE_MID the factor 0.5
+// is dropped: every influence comes out exactly twice the reference's and
+// only their order is ever used (strict comparisons between the three
+// dimensions, narrowphase.cpp:169-177).  Exact on the Fast path: lo + hi is 0
+// or a multiple of ulp(1e-250) (|bounds| >= 1e-250 after widening), so
+// neither the halving nor the halved differences can be subnormal, and
+// rn((a - b) / 2) = rn(a - b) / 2 without underflow; |sums| <= 2^1007.
+__device__ __forceinline__ double pair_mid(I f)
+{
+#if CCDK_TWICE_MID
+    return __dadd_rn(f.lo, f.hi);
+#else
+    return mid2(f);
+#endif
+}
 
 template <int D, class Pts>
 __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const PairBox& b, int c, I rng[2],
@@ -439,7 +458,7 @@ __device__ __forceinline__ void component_pair(bool vf, const Pts& P, const Pair
         // never +/-0), so the grouping is bit-identical to the corner fold.
         auto corner = [&](int iu, int iv) -> I {
             const I f = sub<W>(su[iu], vt[iv]);
-            m[iu * NV + iv] = mid2(f);
+            m[iu * NV + iv] = pair_mid(f);
             return f;
         };
         auto hull = [](I& acc, const I& f) {
