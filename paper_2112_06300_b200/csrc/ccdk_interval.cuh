@@ -362,7 +362,7 @@ __device__ __forceinline__ int process_one(bool vf, const Pts& P, const Box& b,
 // Samples: dim D holds (lo, mid, hi), the others (lo, hi); child 0 takes
 // indices {0, 1} along D, child 1 {1, 2}.
 #ifndef CCDK_TWICE_MID
-#define CCDK_TWICE_MID 0
+#define CCDK_TWICE_MID 1
 #endif
 #ifndef CCDK_SLICE_HULL
 #define CCDK_SLICE_HULL 1
