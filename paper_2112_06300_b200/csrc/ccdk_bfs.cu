@@ -1308,7 +1308,12 @@ bool run_once(Ctx& c, const NarrowIn& in, uint64_t n, const uint8_t* kind, const
     const unsigned gen_grid = static_cast<unsigned>(c.gen_blocks_per_sm * c.num_sms);
     const unsigned gen0_grid = static_cast<unsigned>(std::min<uint64_t>((n + kGenBlock - 1) / kGenBlock,
                                                                         uint64_t(8) * c.num_sms));
-    const unsigned fin_grid = static_cast<unsigned>(c.num_sms);
+    // k_finish blocks (CCDK_FIN_BLOCKS: A/B switch; default one per SM)
+    static const unsigned fin_env = [] {
+        const char* e = std::getenv("CCDK_FIN_BLOCKS");
+        return e && *e ? static_cast<unsigned>(std::strtoul(e, nullptr, 10)) : 0u;
+    }();
+    const unsigned fin_grid = fin_env ? fin_env : static_cast<unsigned>(c.num_sms);
 
     if (c.exp && c.exp->pending)
         export_issue(c); // candidate export D2H runs under the generations
