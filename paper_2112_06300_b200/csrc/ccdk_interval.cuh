@@ -591,8 +591,9 @@ __device__ __forceinline__ PairOutcome process_pair(bool vf, const Pts& P, const
             if (rng[ch].lo > d || rng[ch].hi < -d)
                 alive[ch] = false;
             inside[ch] = inside[ch] && rng[ch].lo >= -d && rng[ch].hi <= d;
-            const double w = __dsub_rn(rng[ch].hi, rng[ch].lo);
-            wmax[ch] = c == 0 ? w : smax(wmax[ch], w);
+            // widths are >= +0 here (no NaN, hi >= lo), so folding from the
+            // initial 0.0 equals starting at component 0 without a select
+            wmax[ch] = smax(wmax[ch], __dsub_rn(rng[ch].hi, rng[ch].lo));
         }
         if (!alive[0] && !alive[1])
             return o;
